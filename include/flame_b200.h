@@ -1,0 +1,113 @@
+/*
+ * flame_b200.h — C ABI of the B200-native FLAME SUMI-ranker hot path.
+ *
+ * This is the drop-in boundary under the reference's Python operator API.
+ * Each entry point replaces one piece of the reference hot path
+ * (paths relative to the reference's pkg/src/flameserve/):
+ *
+ *   flame_create / flame_create_flmp
+ *       replace  model/params.py:77-109  init_params / :154-207 load_params as
+ *       the weight source of model_forward: the caller passes the fp64 arrays
+ *       in iter_param_arrays order (model/params.py:112-128) or a whole FLMP
+ *       file image; the library repacks them into padded, transposed (K-major)
+ *       bf16 or fp32 device tensors.
+ *   flame_set_table
+ *       replaces the per-id feature lookup behind Service.resolve_embeddings
+ *       (service.py:97-108, store.py:59-78) with a device-resident embedding
+ *       table (row = item id; unknown ids decode to zero rows).
+ *   flame_exec_create
+ *       replaces orchestrator.py:104-133 Executor: a fixed-shape compute slot
+ *       with buffers allocated once (zero steady-state allocations) bound to a
+ *       run closure.  Shape = (R requests, hb_bkt history rows per
+ *       request-block, c_bkt candidate rows per request).
+ *   flame_exec_run / flame_exec_capture / flame_exec_replay
+ *       replace Executor.bound_run -> model/forward.py:186-204 model_forward
+ *       (mode FLAME_INPUT_EMBEDDINGS) and Service.resolve_embeddings +
+ *       model_forward (mode FLAME_INPUT_IDS); FLAME_INPUT_GATHER_ONLY runs only
+ *       the PDA feature assembly (np.unique maps + rows).  capture/replay
+ *       record the same launches once into a CUDA graph and replay it.
+ *
+ * Conventions: 0 = ok, 1 = bad argument (Python maps to ValueError),
+ * 2 = CUDA error (RuntimeError).  flame_last_error() describes the last
+ * failure of the calling thread.  All work is stream-ordered on the stream
+ * passed in (a cudaStream_t, or NULL for the legacy default stream).  The
+ * context owns weights and workspace; the caller owns every I/O buffer bound
+ * in FlameIO.  One context per device; threads may share a context as long as
+ * each drives its own executor.
+ */
+#ifndef FLAME_B200_H
+#define FLAME_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct FlameCtx FlameCtx;
+typedef struct FlameExec FlameExec;
+
+/* Mirrors model/config.py:9-19 ModelConfig field for field. */
+typedef struct FlameModelDesc {
+  int hidden_dim;
+  int head_dim;
+  int num_blocks;
+  int layers_per_block;
+  int ffn_dim;
+  int num_tasks;
+  int max_history_len;
+  int max_candidates;
+  unsigned long long seed;
+} FlameModelDesc;
+
+enum FlamePrecision { FLAME_BF16 = 0, FLAME_FP32 = 1 };
+enum FlameInputMode { FLAME_INPUT_EMBEDDINGS = 0, FLAME_INPUT_IDS = 1, FLAME_INPUT_GATHER_ONLY = 2 };
+enum FlameTableDtype { FLAME_TABLE_BF16 = 0, FLAME_TABLE_FP32 = 1 };
+
+/* Caller-owned device buffers bound to an executor.  Unused ones may be NULL
+ * (e.g. the id buffers when only embeddings are scored). Shapes use the
+ * executor's R / H_bkt = num_blocks*hb_bkt / C_bkt = c_bkt. */
+typedef struct FlameIO {
+  const float* hist_emb;      /* [R][H_bkt][hidden_dim] fp32 */
+  const float* cand_emb;      /* [R][C_bkt][hidden_dim] fp32 */
+  const long long* hist_ids;  /* [R][H_bkt] int64 */
+  const long long* cand_ids;  /* [R][C_bkt] int64 */
+  const int* hist_len;        /* [R] actual history length H_r (multiple of num_blocks) */
+  const int* cand_len;        /* [R] actual candidate count C_r (1..C_bkt) */
+  const int* out_offset;      /* [R] first output row of request r */
+  float* scores;              /* [sum C_r][num_tasks] fp32 */
+  long long* unique_ids;      /* [2R][cap] per list: np.unique values (lists: R history, then R candidate) */
+  long long* inverse;         /* [2R][cap] per list: np.unique inverse */
+  int* n_unique;              /* [2R] */
+} FlameIO;
+
+int flame_create(const FlameModelDesc* cfg, const double* weights_fp64, long long n_values,
+                 int precision, int device, FlameCtx** out);
+int flame_create_flmp(const void* flmp_bytes, long long n_bytes, int precision, int device,
+                      FlameCtx** out);
+int flame_destroy(FlameCtx* ctx);
+int flame_set_table(FlameCtx* ctx, const float* host_table, long long num_items, int table_dtype);
+
+/* Capacity of one id list in the unique/inverse buffers: max(H_bkt, C_bkt). */
+int flame_exec_list_capacity(int num_blocks, int hb_bkt, int c_bkt);
+int flame_exec_create(FlameCtx* ctx, int R, int hb_bkt, int c_bkt, const FlameIO* io,
+                      FlameExec** out);
+int flame_exec_destroy(FlameExec* ex);
+int flame_exec_run(FlameExec* ex, int input_mode, void* stream);
+int flame_exec_capture(FlameExec* ex, int input_mode, void* stream);
+int flame_exec_replay(FlameExec* ex, void* stream);
+/* Number of kernel launches one run issues (for the bench's gpu_launches). */
+int flame_exec_launch_count(FlameExec* ex, int input_mode);
+/* Device pointer of an internal workspace tensor, for parity debugging:
+ * "Eh", "Ec" (assembled fp32 rows), "qkv", "attn", "fused". */
+void* flame_exec_workspace(FlameExec* ex, const char* name);
+
+/* Synchronous device-to-host copy (test / debugging helper). */
+int flame_copy_to_host(void* dst_host, const void* src_device, long long bytes);
+
+const char* flame_last_error(void);
+int flame_device_sm_count(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLAME_B200_H */

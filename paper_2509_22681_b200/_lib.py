@@ -1,0 +1,89 @@
+"""ctypes binding of the C ABI declared in include/flame_b200.h.
+
+There is no fallback: if the sm_100a library is missing or fails to load, every
+entry point raises ``RuntimeError`` — the product path never degrades to a CPU
+or PyTorch implementation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_flame_b200.so"
+
+FLAME_BF16, FLAME_FP32 = 0, 1
+INPUT_EMBEDDINGS, INPUT_IDS, INPUT_GATHER_ONLY = 0, 1, 2
+TABLE_BF16, TABLE_FP32 = 0, 1
+
+EXPORTED = (
+    "flame_create", "flame_create_flmp", "flame_destroy", "flame_set_table",
+    "flame_exec_list_capacity", "flame_exec_create", "flame_exec_destroy", "flame_exec_run",
+    "flame_exec_capture", "flame_exec_replay", "flame_exec_launch_count", "flame_exec_workspace",
+    "flame_last_error", "flame_device_sm_count", "flame_copy_to_host",
+)
+
+
+class FlameModelDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "hidden_dim", "head_dim", "num_blocks", "layers_per_block", "ffn_dim", "num_tasks",
+        "max_history_len", "max_candidates")] + [("seed", ctypes.c_ulonglong)]
+
+
+class FlameIO(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "hist_emb", "cand_emb", "hist_ids", "cand_ids", "hist_len", "cand_len", "out_offset",
+        "scores", "unique_ids", "inverse", "n_unique")]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"FLAME sm_100a library not built ({LIB_PATH}); run "
+                "`python -m paper_2509_22681_b200.build` — there is no CPU fallback")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        P, I, LL = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong
+        sig = {
+            "flame_create": (I, [ctypes.POINTER(FlameModelDesc), P, LL, I, I, ctypes.POINTER(P)]),
+            "flame_create_flmp": (I, [P, LL, I, I, ctypes.POINTER(P)]),
+            "flame_destroy": (I, [P]),
+            "flame_set_table": (I, [P, P, LL, I]),
+            "flame_exec_list_capacity": (I, [I, I, I]),
+            "flame_exec_create": (I, [P, I, I, I, ctypes.POINTER(FlameIO), ctypes.POINTER(P)]),
+            "flame_exec_destroy": (I, [P]),
+            "flame_exec_run": (I, [P, I, P]),
+            "flame_exec_capture": (I, [P, I, P]),
+            "flame_exec_replay": (I, [P, P]),
+            "flame_exec_launch_count": (I, [P, I]),
+            "flame_exec_workspace": (P, [P, ctypes.c_char_p]),
+            "flame_last_error": (ctypes.c_char_p, []),
+            "flame_device_sm_count": (I, [I]),
+            "flame_copy_to_host": (I, [P, P, LL]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    """Map C status codes to the reference's exception types."""
+    if rc == 0:
+        return
+    msg = (load().flame_last_error() or b"").decode(errors="replace")
+    if rc == 1:
+        raise ValueError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,794 @@
+// B200-native FLAME runtime: weight repacking, executors (fixed-shape
+// workspace + CUDA graph), and the per-batch launch sequence of the
+// SUMI-ranker forward pass.  See include/flame_b200.h for the C ABI.
+//
+// Data layout in HBM for one executor (R requests, N_b = G Climber blocks):
+//   row space of block g:  [ R*hb_bkt history rows | R*c_bkt candidate rows ]
+//   Eh  fp32 [G][R*hb_bkt][D]   history embeddings, block-major (PDA output)
+//   Ec  fp32 [R*c_bkt][D]       candidate embeddings, shared by all blocks
+//   Y   act  [G][rows][D]       LayerNorm output (GEMM A operand)
+//   QKV act  [G][rows][3*DA]    projections; head h at columns h*64 of Q | K | V
+//   AO  act  [G][rows][DA]      attention output
+//   X1  fp32 [G][rows][D]       residual stream after attention
+//   Hf  act  [G][rows][F]       FFN hidden (GELU applied)
+//   Xa/Xb fp32 [G][rows][D]     residual stream after the FFN (ping-pong over layers)
+//   Fz  act  [R*c_bkt][D]       gated fusion, He act [R*c_bkt][F] expert hidden
+// act = bf16 (FLAME_BF16) or fp32 (FLAME_FP32 verification mode).
+// D = pad64(d), DA = heads * 64 (each head padded to 64 lanes), F = pad64(f).
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/flame_b200.h"
+#include "ptx.cuh"
+#include "common.cuh"
+#include "gemm_tcgen05.cuh"
+#include "gemm_launch.cuh"
+#include "attention_tcgen05.cuh"
+#include "simt_f32.cuh"
+#include "rowops.cuh"
+#include "pda.cuh"
+
+using namespace flame;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      return fail(2, std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+inline int pad_to(int x, int m) { return (x + m - 1) / m * m; }
+
+struct LayerW {
+  void* wqkv = nullptr;  // [G][3DA][D]
+  void* wo = nullptr;    // [G][D][DA]
+  void* w1 = nullptr;    // [G][F][D]
+  void* w2 = nullptr;    // [G][D][F]
+  float* b1 = nullptr;   // [G][F]
+  float* b2 = nullptr;   // [G][D]
+  float* ln1_g = nullptr;
+  float* ln1_b = nullptr;
+  float* ln2_g = nullptr;
+  float* ln2_b = nullptr;  // [G][D]
+};
+
+}  // namespace
+
+struct FlameCtx {
+  FlameModelDesc cfg{};
+  int precision = FLAME_BF16;
+  int device = 0;
+  int num_sms = 148;
+  int d = 0, dh = 0, nh = 0, G = 0, L = 0, f = 0, tasks = 0;
+  int D = 0, DA = 0, F = 0;
+  size_t act_bytes = 2;
+  std::vector<LayerW> layers;
+  float* gate_w = nullptr;  // [G][D]
+  float* gate_b = nullptr;
+  void* we1 = nullptr;      // [F][D]
+  float* be1 = nullptr;     // [F]
+  float* we2 = nullptr;     // [F][tasks]
+  float* be2 = nullptr;     // [tasks]
+  float* scale = nullptr;       // [G] 1/(tau sqrt(dh))
+  float* scale_log2 = nullptr;  // [G] log2(e)/(tau sqrt(dh))
+  void* table = nullptr;
+  long long num_items = 0;
+  int table_dtype = FLAME_TABLE_FP32;
+  std::vector<void*> allocs;
+
+  ~FlameCtx() {
+    for (void* p : allocs) cudaFree(p);
+  }
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, count * sizeof(T) > 0 ? count * sizeof(T) : 16) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+struct FlameExec {
+  FlameCtx* ctx = nullptr;
+  int R = 0, hb_bkt = 0, c_bkt = 0, H_bkt = 0, cap = 0;
+  long long Rh = 0, Rc = 0, rows = 0;
+  FlameIO io{};
+  float* Eh = nullptr;
+  float* Ec = nullptr;
+  void* Y = nullptr;
+  void* QKV = nullptr;
+  void* AO = nullptr;
+  float* X1 = nullptr;
+  void* Hf = nullptr;
+  float* Xa = nullptr;
+  float* Xb = nullptr;
+  void* Fz = nullptr;
+  void* He = nullptr;
+  int* spos = nullptr;
+  int* ustart = nullptr;
+  long long* unique_ws = nullptr;
+  long long* inverse_ws = nullptr;
+  int* nuniq_ws = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_mode = -1;
+  int launches = 0;
+  std::vector<void*> allocs;
+
+  ~FlameExec() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (void* p : allocs) cudaFree(p);
+  }
+  void* alloc_bytes(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, n > 0 ? n : 16) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return p;
+  }
+};
+
+// ----------------------------------------------------------------- weights
+namespace {
+
+// Reads the fp64 stream in iter_param_arrays order (model/params.py:112-128).
+struct Cursor {
+  const double* p;
+  long long left;
+  bool take(long long n, const double** out) {
+    if (n > left) return false;
+    *out = p;
+    p += n;
+    left -= n;
+    return true;
+  }
+};
+
+template <typename T>
+T cvt(double v);
+template <>
+float cvt<float>(double v) { return static_cast<float>(v); }
+template <>
+__nv_bfloat16 cvt<__nv_bfloat16>(double v) { return __float2bfloat16_rn(static_cast<float>(v)); }
+
+// Transposed, padded weight: dst[n_out][k_in] (K-major) from src[k][n] row-major (in,out).
+// out_map / in_map give the padded index of each logical output / input index.
+template <typename T>
+void pack_transposed(std::vector<T>& dst, size_t dst_off, int rows_pad, int cols_pad,
+                     const double* src, int k_in, int n_out, const std::vector<int>& out_map,
+                     const std::vector<int>& in_map) {
+  (void)rows_pad;
+  for (int k = 0; k < k_in; ++k)
+    for (int n = 0; n < n_out; ++n)
+      dst[dst_off + static_cast<size_t>(out_map[n]) * cols_pad + in_map[k]] = cvt<T>(src[static_cast<size_t>(k) * n_out + n]);
+}
+
+template <typename T>
+int upload_weights(FlameCtx* c, const double* w, long long n_values) {
+  const int d = c->d, f = c->f, G = c->G, L = c->L, D = c->D, DA = c->DA, F = c->F, dh = c->dh,
+            nh = c->nh, tasks = c->tasks;
+  std::vector<int> id_d(d), id_f(f), head_map(d);
+  for (int i = 0; i < d; ++i) id_d[i] = i;
+  for (int i = 0; i < f; ++i) id_f[i] = i;
+  for (int hh = 0; hh < nh; ++hh)
+    for (int j = 0; j < dh; ++j) head_map[hh * dh + j] = hh * 64 + j;
+  // per-layer host staging, all blocks stacked
+  struct HostLayer {
+    std::vector<T> wqkv, wo, w1, w2;
+    std::vector<float> b1, b2, l1g, l1b, l2g, l2b;
+  };
+  std::vector<HostLayer> hl(L);
+  for (auto& h : hl) {
+    h.wqkv.assign(static_cast<size_t>(G) * 3 * DA * D, cvt<T>(0.0));
+    h.wo.assign(static_cast<size_t>(G) * D * DA, cvt<T>(0.0));
+    h.w1.assign(static_cast<size_t>(G) * F * D, cvt<T>(0.0));
+    h.w2.assign(static_cast<size_t>(G) * D * F, cvt<T>(0.0));
+    h.b1.assign(static_cast<size_t>(G) * F, 0.f);
+    h.b2.assign(static_cast<size_t>(G) * D, 0.f);
+    h.l1g.assign(static_cast<size_t>(G) * D, 0.f);
+    h.l1b = h.l1g;
+    h.l2g = h.l1g;
+    h.l2b = h.l1g;
+  }
+  std::vector<float> gate_w(static_cast<size_t>(G) * D, 0.f), gate_b(gate_w.size(), 0.f);
+  std::vector<float> scale(G), scale_log2(G);
+  Cursor cur{w, n_values};
+  const double* a;
+  auto need = [&](long long n) {
+    if (!cur.take(n, &a)) return false;
+    return true;
+  };
+  std::vector<int> qmap(d), kmap(d), vmap(d);
+  for (int i = 0; i < d; ++i) {
+    qmap[i] = head_map[i];
+    kmap[i] = DA + head_map[i];
+    vmap[i] = 2 * DA + head_map[i];
+  }
+  for (int b = 0; b < G; ++b) {
+    for (int l = 0; l < L; ++l) {
+      HostLayer& h = hl[l];
+      const size_t qkv_off = static_cast<size_t>(b) * 3 * DA * D;
+      if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_q)");
+      pack_transposed(h.wqkv, qkv_off, 3 * DA, D, a, d, d, qmap, id_d);
+      if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_k)");
+      pack_transposed(h.wqkv, qkv_off, 3 * DA, D, a, d, d, kmap, id_d);
+      if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_v)");
+      pack_transposed(h.wqkv, qkv_off, 3 * DA, D, a, d, d, vmap, id_d);
+      if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_o)");
+      pack_transposed(h.wo, static_cast<size_t>(b) * D * DA, D, DA, a, d, d, id_d, head_map);
+      float* lnv[4] = {h.l1g.data(), h.l1b.data(), h.l2g.data(), h.l2b.data()};
+      for (int q = 0; q < 4; ++q) {
+        if (!need(d)) return fail(1, "weights too short (ln)");
+        for (int i = 0; i < d; ++i) lnv[q][static_cast<size_t>(b) * D + i] = static_cast<float>(a[i]);
+      }
+      if (!need(static_cast<long long>(d) * f)) return fail(1, "weights too short (w1)");
+      pack_transposed(h.w1, static_cast<size_t>(b) * F * D, F, D, a, d, f, id_f, id_d);
+      if (!need(f)) return fail(1, "weights too short (b1)");
+      for (int i = 0; i < f; ++i) h.b1[static_cast<size_t>(b) * F + i] = static_cast<float>(a[i]);
+      if (!need(static_cast<long long>(f) * d)) return fail(1, "weights too short (w2)");
+      pack_transposed(h.w2, static_cast<size_t>(b) * D * F, D, F, a, f, d, id_d, id_f);
+      if (!need(d)) return fail(1, "weights too short (b2)");
+      for (int i = 0; i < d; ++i) h.b2[static_cast<size_t>(b) * D + i] = static_cast<float>(a[i]);
+    }
+    if (!need(1)) return fail(1, "weights too short (temperature)");
+    const double tau = a[0];
+    if (!(tau > 0)) return fail(1, "block temperature must be positive");
+    const double sc = 1.0 / (tau * std::sqrt(static_cast<double>(dh)));
+    scale[b] = static_cast<float>(sc);
+    scale_log2[b] = static_cast<float>(sc * 1.4426950408889634);
+    if (!need(d)) return fail(1, "weights too short (gate_weight)");
+    for (int i = 0; i < d; ++i) gate_w[static_cast<size_t>(b) * D + i] = static_cast<float>(a[i]);
+    if (!need(d)) return fail(1, "weights too short (gate_bias)");
+    for (int i = 0; i < d; ++i) gate_b[static_cast<size_t>(b) * D + i] = static_cast<float>(a[i]);
+  }
+  std::vector<T> we1(static_cast<size_t>(F) * D, cvt<T>(0.0));
+  std::vector<float> be1(F, 0.f), we2(static_cast<size_t>(F) * tasks, 0.f), be2(tasks, 0.f);
+  if (!need(static_cast<long long>(d) * f)) return fail(1, "weights too short (expert_w1)");
+  pack_transposed(we1, 0, F, D, a, d, f, id_f, id_d);
+  if (!need(f)) return fail(1, "weights too short (expert_b1)");
+  for (int i = 0; i < f; ++i) be1[i] = static_cast<float>(a[i]);
+  if (!need(static_cast<long long>(f) * tasks)) return fail(1, "weights too short (expert_w2)");
+  for (int k = 0; k < f; ++k)
+    for (int t = 0; t < tasks; ++t) we2[static_cast<size_t>(k) * tasks + t] = static_cast<float>(a[static_cast<size_t>(k) * tasks + t]);
+  if (!need(tasks)) return fail(1, "weights too short (expert_b2)");
+  for (int t = 0; t < tasks; ++t) be2[t] = static_cast<float>(a[t]);
+  if (cur.left != 0) return fail(1, "trailing values in weight stream (" + std::to_string(cur.left) + ")");
+
+  auto up = [&](auto& vec, auto** dst) -> bool {
+    using E = typename std::remove_reference<decltype(vec)>::type::value_type;
+    E* p = c->alloc<E>(vec.size());
+    if (!p) return false;
+    if (cudaMemcpy(p, vec.data(), vec.size() * sizeof(E), cudaMemcpyHostToDevice) != cudaSuccess) return false;
+    *dst = p;
+    return true;
+  };
+  c->layers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    HostLayer& h = hl[l];
+    LayerW& lw = c->layers[l];
+    T *wqkv, *wo, *w1, *w2;
+    if (!up(h.wqkv, &wqkv) || !up(h.wo, &wo) || !up(h.w1, &w1) || !up(h.w2, &w2) ||
+        !up(h.b1, &lw.b1) || !up(h.b2, &lw.b2) || !up(h.l1g, &lw.ln1_g) || !up(h.l1b, &lw.ln1_b) ||
+        !up(h.l2g, &lw.ln2_g) || !up(h.l2b, &lw.ln2_b))
+      return fail(2, "device allocation / copy of layer weights failed");
+    lw.wqkv = wqkv; lw.wo = wo; lw.w1 = w1; lw.w2 = w2;
+  }
+  T* we1d;
+  if (!up(gate_w, &c->gate_w) || !up(gate_b, &c->gate_b) || !up(we1, &we1d) || !up(be1, &c->be1) ||
+      !up(we2, &c->we2) || !up(be2, &c->be2) || !up(scale, &c->scale) || !up(scale_log2, &c->scale_log2))
+    return fail(2, "device allocation / copy of model weights failed");
+  c->we1 = we1d;
+  return 0;
+}
+
+int validate_desc(const FlameModelDesc& m) {
+  // model/config.py:20-42
+  if (m.hidden_dim < 1 || m.head_dim < 1 || m.num_blocks < 1 || m.layers_per_block < 1 ||
+      m.ffn_dim < 1 || m.num_tasks < 1 || m.max_history_len < 1 || m.max_candidates < 1)
+    return fail(1, "all model dims must be >= 1");
+  if (m.hidden_dim % m.head_dim != 0) return fail(1, "head_dim must divide hidden_dim");
+  if (m.max_history_len % m.num_blocks != 0) return fail(1, "num_blocks must divide max_history_len");
+  if (m.head_dim > 64) return fail(1, "head_dim > 64 is not supported by the attention kernels");
+  if (m.num_tasks > 8) return fail(1, "num_tasks > 8 is not supported by the expert kernel");
+  if (pad_to(m.hidden_dim, 64) > 1024 || m.hidden_dim / m.head_dim * 64 > 4096)
+    return fail(1, "hidden_dim too large for the row kernels");
+  return 0;
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- pipeline
+namespace {
+
+template <typename Act>
+struct Pipe {
+  FlameExec* e;
+  FlameCtx* c;
+  cudaStream_t s;
+  int launches = 0;
+
+  Act* act(void* p) { return static_cast<Act*>(p); }
+
+  int check() {
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return fail(2, std::string("kernel launch: ") + cudaGetErrorString(err));
+    ++launches;
+    return 0;
+  }
+
+  int gemm(const Act* A, long long lda, long long a_gstride, int a_shared, const Act* W, long long ldw,
+           long long w_gstride, int M, int N, int K, int G, void* out, long long out_ld,
+           long long out_gstride, int out_col0, const float* bias, long long bias_gstride,
+           const float* resid, long long resid_ld, long long resid_gstride, int epi) {
+    GemmEpilogue ep{};
+    ep.out = out; ep.out_ld = out_ld; ep.out_gstride = out_gstride; ep.out_col0 = out_col0;
+    ep.bias = bias; ep.bias_gstride = bias_gstride;
+    ep.resid = resid; ep.resid_ld = resid_ld; ep.resid_gstride = resid_gstride;
+    ep.M = M; ep.N = N;
+    if (M <= 0) return 0;
+    if constexpr (std::is_same<Act, __nv_bfloat16>::value) {
+      GemmProblem p{};
+      p.A = A; p.lda = lda; p.a_gstride = a_gstride; p.a_shared = a_shared;
+      p.W = W; p.ldw = ldw; p.w_gstride = w_gstride;
+      p.M = M; p.N = N; p.K = K; p.G = G; p.ep = ep; p.epi = epi;
+      cudaError_t err = launch_gemm(p, s, c->num_sms);
+      if (err != cudaSuccess) return fail(2, std::string("tcgen05 gemm: ") + cudaGetErrorString(err));
+      ++launches;
+      return 0;
+    } else {
+      epi |= EPI_OUT_F32;  // verification mode keeps every activation in fp32
+      dim3 grid((N + 127) / 128, (M + 127) / 128, G);
+      const long long ag = a_shared ? 0 : a_gstride;
+#define F32_GEMM(E) gemm_f32_simt<E><<<grid, 256, 0, s>>>(A, lda, ag, W, ldw, w_gstride, M, N, K, ep)
+      switch (epi) {
+        case 0: F32_GEMM(0); break;
+        case EPI_OUT_F32: F32_GEMM(EPI_OUT_F32); break;
+        case EPI_BIAS | EPI_GELU: F32_GEMM(EPI_BIAS | EPI_GELU); break;
+        case EPI_BIAS | EPI_GELU | EPI_OUT_F32: F32_GEMM(EPI_BIAS | EPI_GELU | EPI_OUT_F32); break;
+        case EPI_RESID | EPI_OUT_F32: F32_GEMM(EPI_RESID | EPI_OUT_F32); break;
+        case EPI_BIAS | EPI_RESID | EPI_OUT_F32: F32_GEMM(EPI_BIAS | EPI_RESID | EPI_OUT_F32); break;
+        default: return fail(1, "unsupported fp32 epilogue");
+      }
+#undef F32_GEMM
+      return check();
+    }
+  }
+
+  int layer_norm(const float* src, long long src_ld, long long src_gstride, Act* out, long long out_ld,
+                 long long out_gstride, const float* gamma, const float* beta, long long rows) {
+    if (rows <= 0) return 0;
+    const int threads = 256;
+    dim3 grid(static_cast<unsigned>((rows * 32 + threads - 1) / threads), c->G);
+    layer_norm_rows<Act><<<grid, threads, 0, s>>>(src, src_ld, src_gstride, out, out_ld, out_gstride,
+                                                  gamma, beta, static_cast<int>(rows), c->D, c->d);
+    return check();
+  }
+
+  int attention(bool hist) {
+    const int tiles = hist ? (e->hb_bkt + 127) / 128 : (e->c_bkt + 127) / 128;
+    if (tiles == 0 || e->R == 0) return 0;
+    dim3 grid(tiles, c->nh, c->G * e->R);
+    if constexpr (std::is_same<Act, __nv_bfloat16>::value) {
+      AttnArgs a{};
+      a.qkv = act(e->QKV); a.out = act(e->AO);
+      a.qkv_gstride = e->rows * 3LL * c->DA;
+      a.out_ld = c->DA; a.out_gstride = e->rows * static_cast<long long>(c->DA);
+      a.DA = c->DA; a.R = e->R; a.hb_bkt = e->hb_bkt; a.c_bkt = e->c_bkt; a.num_blocks = c->G;
+      a.hist_len = e->io.hist_len; a.cand_len = e->io.cand_len; a.scale_log2 = c->scale_log2;
+      CUtensorMap tm;
+      if (!make_tmap_bf16_3d(&tm, e->QKV, 3ULL * c->DA, e->rows, c->G, 3ULL * c->DA * 2,
+                             e->rows * 3ULL * c->DA * 2, 64, 128))
+        return fail(2, "tensor map for QKV failed");
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(sumi_attention_tcgen05<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes);
+        cudaFuncSetAttribute(sumi_attention_tcgen05<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes);
+        attr = true;
+      }
+      if (hist)
+        sumi_attention_tcgen05<true><<<grid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
+      else
+        sumi_attention_tcgen05<false><<<grid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
+    } else {
+      AttnArgsF32 a{};
+      a.qkv = act(e->QKV); a.out = act(e->AO);
+      a.qkv_gstride = e->rows * 3LL * c->DA;
+      a.out_ld = c->DA; a.out_gstride = e->rows * static_cast<long long>(c->DA);
+      a.DA = c->DA; a.R = e->R; a.hb_bkt = e->hb_bkt; a.c_bkt = e->c_bkt; a.num_blocks = c->G;
+      a.hist_len = e->io.hist_len; a.cand_len = e->io.cand_len; a.scale = c->scale;
+      if (hist)
+        sumi_attention_f32<true><<<grid, 128, 0, s>>>(a);
+      else
+        sumi_attention_f32<false><<<grid, 128, 0, s>>>(a);
+    }
+    return check();
+  }
+
+  int assemble(int mode) {
+    if (mode == FLAME_INPUT_EMBEDDINGS) {
+      if (!e->io.hist_emb || !e->io.cand_emb) return fail(1, "embedding inputs not bound");
+      const long long warps = static_cast<long long>(c->G) * e->Rh + e->Rc;
+      const int threads = 256;
+      scatter_embeddings<<<static_cast<unsigned>((warps * 32 + threads - 1) / threads), threads, 0, s>>>(
+          e->io.hist_emb, e->io.cand_emb, c->d, c->D, e->R, e->H_bkt, e->c_bkt, c->G, e->hb_bkt,
+          e->io.hist_len, e->io.cand_len, e->Eh, e->Ec);
+      return check();
+    }
+    if (!e->io.hist_ids || !e->io.cand_ids) return fail(1, "id inputs not bound");
+    if (!c->table) return fail(1, "no embedding table set (flame_set_table)");
+    PdaLists l{};
+    l.hist_ids = e->io.hist_ids; l.cand_ids = e->io.cand_ids;
+    l.hist_len = e->io.hist_len; l.cand_len = e->io.cand_len;
+    l.R = e->R; l.H_bkt = e->H_bkt; l.C_bkt = e->c_bkt;
+    l.unique = e->io.unique_ids ? e->io.unique_ids : e->unique_ws;
+    l.inverse = e->io.inverse ? e->io.inverse : e->inverse_ws;
+    l.n_unique = e->io.n_unique ? e->io.n_unique : e->nuniq_ws;
+    l.spos = e->spos; l.ustart = e->ustart; l.cap = e->cap;
+    int P = 1;
+    while (P < e->cap) P <<= 1;
+    const int smem = P * 16;
+    static int smem_set = 0;
+    if (smem > smem_set) {
+      cudaFuncSetAttribute(pda_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      smem_set = smem;
+    }
+    pda_dedup<<<2 * e->R, kPdaThreads, smem, s>>>(l);
+    if (int rc = check()) return rc;
+    {
+      PdaGatherArgs g{};
+      g.l = l; g.table = c->table; g.num_items = c->num_items; g.D = c->D; g.G = c->G;
+      g.hb_bkt = e->hb_bkt; g.Eh = e->Eh; g.Ec = e->Ec;
+      int bx = (c->num_sms * 8 + 2 * e->R - 1) / (2 * e->R);
+      if (bx < 1) bx = 1;
+      const int max_bx = (e->cap + 7) / 8;
+      if (bx > max_bx) bx = max_bx < 1 ? 1 : max_bx;
+      dim3 grid(bx, 2 * e->R);
+      if (c->table_dtype == FLAME_TABLE_BF16)
+        pda_gather<__nv_bfloat16><<<grid, 256, 0, s>>>(g);
+      else
+        pda_gather<float><<<grid, 256, 0, s>>>(g);
+      if (int rc = check()) return rc;
+    }
+    return 0;
+  }
+
+  int run(int mode) {
+    if (int rc = assemble(mode)) return rc;
+    if (mode == FLAME_INPUT_GATHER_ONLY) return 0;
+    const int D = c->D, DA = c->DA, F = c->F, G = c->G;
+    const long long rows = e->rows, Rh = e->Rh, Rc = e->Rc;
+    const long long gD = rows * D, gQKV = rows * 3LL * DA, gA = rows * DA, gF = rows * F;
+    Act* Y = act(e->Y);
+    Act* QKV = act(e->QKV);
+    Act* AO = act(e->AO);
+    Act* Hf = act(e->Hf);
+    float* Xcur = nullptr;  // residual stream input of this layer (null at layer 0)
+    for (int l = 0; l < c->L; ++l) {
+      const LayerW& w = c->layers[l];
+      const bool last = l == c->L - 1;
+      // sources of this layer's input rows
+      const float* src_h = l == 0 ? e->Eh : Xcur;
+      const long long src_h_g = l == 0 ? Rh * D : gD;
+      const float* src_c = l == 0 ? e->Ec : Xcur + Rh * D;
+      const long long src_c_g = l == 0 ? 0 : gD;
+      float* Xnext = (Xcur == e->Xa) ? e->Xb : e->Xa;
+      // LN1 (forward.py:111 / :120)
+      if (int rc = layer_norm(src_h, D, src_h_g, Y, D, gD, w.ln1_g, w.ln1_b, Rh)) return rc;
+      if (int rc = layer_norm(src_c, D, src_c_g, Y + Rh * D, D, gD, w.ln1_g, w.ln1_b, Rc)) return rc;
+      // projections (forward.py:112-114 last layer: history rows K,V only; :121-123 others)
+      const Act* Wqkv = act(w.wqkv);
+      if (last) {
+        if (int rc = gemm(Y, D, gD, 0, Wqkv + static_cast<long long>(DA) * D, D, 3LL * DA * D, Rh, 2 * DA, D, G,
+                          QKV, 3LL * DA, gQKV, DA, nullptr, 0, nullptr, 0, 0, 0)) return rc;
+      } else {
+        if (int rc = gemm(Y, D, gD, 0, Wqkv, D, 3LL * DA * D, Rh, 3 * DA, D, G, QKV, 3LL * DA, gQKV, 0,
+                          nullptr, 0, nullptr, 0, 0, 0)) return rc;
+      }
+      if (int rc = gemm(Y + Rh * D, D, gD, 0, Wqkv, D, 3LL * DA * D, Rc, 3 * DA, D, G, QKV + Rh * 3LL * DA,
+                        3LL * DA, gQKV, 0, nullptr, 0, nullptr, 0, 0, 0)) return rc;
+      // SUMI attention (attention.py:118-146; :149-178 for non-final layers)
+      if (int rc = attention(false)) return rc;
+      if (!last) { if (int rc = attention(true)) return rc; }
+      // O-projection + residual (forward.py:116 / :135)
+      if (int rc = gemm(AO + Rh * DA, DA, gA, 0, act(w.wo), DA, static_cast<long long>(D) * DA, Rc, D, DA, G,
+                        e->X1 + Rh * D, D, gD, 0, nullptr, 0, src_c, D, src_c_g, EPI_RESID | EPI_OUT_F32)) return rc;
+      if (!last) {
+        if (int rc = gemm(AO, DA, gA, 0, act(w.wo), DA, static_cast<long long>(D) * DA, Rh, D, DA, G, e->X1, D, gD, 0,
+                          nullptr, 0, src_h, D, src_h_g, EPI_RESID | EPI_OUT_F32)) return rc;
+      }
+      // LN2 + FFN + residual (forward.py:117-118 / :137-138)
+      const long long r0 = last ? Rh : 0;  // first row of the range that continues
+      const long long nr = last ? Rc : rows;
+      if (int rc = layer_norm(e->X1 + r0 * D, D, gD, Y + r0 * D, D, gD, w.ln2_g, w.ln2_b, nr)) return rc;
+      if (int rc = gemm(Y + r0 * D, D, gD, 0, act(w.w1), D, static_cast<long long>(F) * D, static_cast<int>(nr), F, D, G,
+                        Hf + r0 * F, F, gF, 0, w.b1, F, nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
+      if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F, G,
+                        Xnext + r0 * D, D, gD, 0, w.b2, D, e->X1 + r0 * D, D, gD,
+                        EPI_BIAS | EPI_RESID | EPI_OUT_F32)) return rc;
+      Xcur = Xnext;
+    }
+    // gated fusion over blocks (forward.py:143-156)
+    {
+      const long long n = Rc * (D / 4);
+      gated_fusion_rows<Act><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+          Xcur + Rh * D, D, gD, G, c->gate_w, c->gate_b, act(e->Fz), D, static_cast<int>(Rc), D);
+      if (int rc = check()) return rc;
+    }
+    // expert heads (forward.py:159-166)
+    if (int rc = gemm(act(e->Fz), D, 0, 1, act(c->we1), D, 0, static_cast<int>(Rc), F, D, 1, e->He, F, 0, 0, c->be1, 0,
+                      nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
+    {
+      const long long threads = Rc * 32;
+      expert_out_rows<Act><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+          act(e->He), F, c->we2, c->be2, F, c->tasks, e->c_bkt, e->io.cand_len, e->io.out_offset,
+          e->io.scores, static_cast<int>(Rc));
+      if (int rc = check()) return rc;
+    }
+    return 0;
+  }
+};
+
+int exec_run(FlameExec* e, int mode, cudaStream_t s, int* launches) {
+  if (mode < 0 || mode > 2) return fail(1, "bad input mode");
+  if (mode != FLAME_INPUT_GATHER_ONLY && !e->io.scores) return fail(1, "scores buffer not bound");
+  if (!e->io.hist_len || !e->io.cand_len || !e->io.out_offset) return fail(1, "length buffers not bound");
+  int rc;
+  int n = 0;
+  if (e->ctx->precision == FLAME_BF16) {
+    Pipe<__nv_bfloat16> p{e, e->ctx, s};
+    rc = p.run(mode);
+    n = p.launches;
+  } else {
+    Pipe<float> p{e, e->ctx, s};
+    rc = p.run(mode);
+    n = p.launches;
+  }
+  if (launches) *launches = n;
+  return rc;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* flame_last_error(void) { return g_err.c_str(); }
+
+int flame_copy_to_host(void* dst, const void* src, long long bytes) {
+  CUDA_TRY(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int flame_device_sm_count(int device) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return n;
+}
+
+int flame_create(const FlameModelDesc* cfg, const double* weights, long long n_values, int precision,
+                 int device, FlameCtx** out) {
+  if (!cfg || !weights || !out) return fail(1, "null argument");
+  if (int rc = validate_desc(*cfg)) return rc;
+  if (precision != FLAME_BF16 && precision != FLAME_FP32) return fail(1, "bad precision");
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new FlameCtx();
+  c->cfg = *cfg;
+  c->precision = precision;
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  c->d = cfg->hidden_dim; c->dh = cfg->head_dim; c->nh = cfg->hidden_dim / cfg->head_dim;
+  c->G = cfg->num_blocks; c->L = cfg->layers_per_block; c->f = cfg->ffn_dim; c->tasks = cfg->num_tasks;
+  c->D = pad_to(c->d, 64); c->DA = c->nh * 64; c->F = pad_to(c->f, 64);
+  c->act_bytes = precision == FLAME_BF16 ? 2 : 4;
+  int rc = precision == FLAME_BF16 ? upload_weights<__nv_bfloat16>(c, weights, n_values)
+                                   : upload_weights<float>(c, weights, n_values);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return 0;
+}
+
+int flame_create_flmp(const void* bytes, long long n_bytes, int precision, int device, FlameCtx** out) {
+  // FLMP: b"FLMP" + <11I (version, 8 dims, seed lo, seed hi) + fp64 body (model/params.py:131-147)
+  if (!bytes || n_bytes < 48) return fail(1, "not a model parameter file (too short)");
+  const unsigned char* b = static_cast<const unsigned char*>(bytes);
+  if (std::memcmp(b, "FLMP", 4) != 0) return fail(1, "not a model parameter file (bad magic)");
+  uint32_t h[11];
+  std::memcpy(h, b + 4, sizeof(h));
+  if (h[0] != 1) return fail(1, "unsupported parameter file version " + std::to_string(h[0]));
+  FlameModelDesc m{};
+  m.hidden_dim = static_cast<int>(h[1]); m.head_dim = static_cast<int>(h[2]);
+  m.num_blocks = static_cast<int>(h[3]); m.layers_per_block = static_cast<int>(h[4]);
+  m.ffn_dim = static_cast<int>(h[5]); m.num_tasks = static_cast<int>(h[6]);
+  m.max_history_len = static_cast<int>(h[7]); m.max_candidates = static_cast<int>(h[8]);
+  m.seed = static_cast<unsigned long long>(h[9]) | (static_cast<unsigned long long>(h[10]) << 32);
+  const long long body = n_bytes - 48;
+  if (body % 8 != 0) return fail(1, "parameter file body is not a whole number of float64 values");
+  std::vector<double> w(static_cast<size_t>(body / 8));
+  std::memcpy(w.data(), b + 48, static_cast<size_t>(body));
+  return flame_create(&m, w.data(), static_cast<long long>(w.size()), precision, device, out);
+}
+
+int flame_destroy(FlameCtx* ctx) {
+  delete ctx;
+  return 0;
+}
+
+int flame_set_table(FlameCtx* c, const float* host_table, long long num_items, int dtype) {
+  if (!c || (!host_table && num_items > 0) || num_items < 0) return fail(1, "bad table arguments");
+  if (dtype != FLAME_TABLE_BF16 && dtype != FLAME_TABLE_FP32) return fail(1, "bad table dtype");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t n = static_cast<size_t>(num_items) * c->D;
+  void* dev = nullptr;
+  if (dtype == FLAME_TABLE_BF16) {
+    std::vector<__nv_bfloat16> t(n, __float2bfloat16_rn(0.f));
+    for (long long i = 0; i < num_items; ++i)
+      for (int k = 0; k < c->d; ++k) t[static_cast<size_t>(i) * c->D + k] = __float2bfloat16_rn(host_table[static_cast<size_t>(i) * c->d + k]);
+    dev = c->alloc<__nv_bfloat16>(n);
+    if (!dev) return fail(2, "table allocation failed");
+    CUDA_TRY(cudaMemcpy(dev, t.data(), n * 2, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> t(n, 0.f);
+    for (long long i = 0; i < num_items; ++i)
+      for (int k = 0; k < c->d; ++k) t[static_cast<size_t>(i) * c->D + k] = host_table[static_cast<size_t>(i) * c->d + k];
+    dev = c->alloc<float>(n);
+    if (!dev) return fail(2, "table allocation failed");
+    CUDA_TRY(cudaMemcpy(dev, t.data(), n * 4, cudaMemcpyHostToDevice));
+  }
+  c->table = dev;
+  c->num_items = num_items;
+  c->table_dtype = dtype;
+  return 0;
+}
+
+int flame_exec_list_capacity(int num_blocks, int hb_bkt, int c_bkt) {
+  const int H = num_blocks * hb_bkt;
+  return H > c_bkt ? H : c_bkt;
+}
+
+int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* io, FlameExec** out) {
+  if (!c || !io || !out) return fail(1, "null argument");
+  if (R < 1 || hb_bkt < 0 || c_bkt < 1) return fail(1, "bad executor shape");
+  if (static_cast<long long>(hb_bkt) * c->G > c->cfg.max_history_len)
+    return fail(1, "executor history capacity exceeds max_history_len");
+  if (c_bkt > c->cfg.max_candidates && c_bkt > 128)
+    return fail(1, "executor candidate capacity exceeds max_candidates");
+  const int cap = flame_exec_list_capacity(c->G, hb_bkt, c_bkt);
+  if (cap > kPdaMaxList) return fail(1, "id list longer than the PDA dedup kernel supports");
+  CUDA_TRY(cudaSetDevice(c->device));
+  auto* e = new FlameExec();
+  e->ctx = c;
+  e->R = R; e->hb_bkt = hb_bkt; e->c_bkt = c_bkt; e->H_bkt = hb_bkt * c->G; e->cap = cap;
+  e->Rh = static_cast<long long>(R) * hb_bkt;
+  e->Rc = static_cast<long long>(R) * c_bkt;
+  e->rows = e->Rh + e->Rc;
+  e->io = *io;
+  const size_t ab = c->act_bytes;
+  const size_t G = c->G, rows = e->rows, D = c->D, DA = c->DA, F = c->F;
+  bool ok = true;
+  auto A = [&](size_t bytes) {
+    void* p = e->alloc_bytes(bytes);
+    ok = ok && p != nullptr;
+    return p;
+  };
+  e->Eh = static_cast<float*>(A(G * e->Rh * D * 4));
+  e->Ec = static_cast<float*>(A(e->Rc * D * 4));
+  e->Y = A(G * rows * D * ab);
+  e->QKV = A(G * rows * 3 * DA * ab);
+  e->AO = A(G * rows * DA * ab);
+  e->X1 = static_cast<float*>(A(G * rows * D * 4));
+  e->Hf = A(G * rows * F * ab);
+  e->Xa = static_cast<float*>(A(G * rows * D * 4));
+  e->Xb = c->L > 1 ? static_cast<float*>(A(G * rows * D * 4)) : nullptr;
+  e->Fz = A(e->Rc * D * ab);
+  e->He = A(e->Rc * F * ab);
+  e->spos = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
+  e->ustart = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
+  e->unique_ws = static_cast<long long*>(A(2 * static_cast<size_t>(R) * cap * 8));
+  e->inverse_ws = static_cast<long long*>(A(2 * static_cast<size_t>(R) * cap * 8));
+  e->nuniq_ws = static_cast<int*>(A(2 * static_cast<size_t>(R) * 4));
+  if (!ok) {
+    delete e;
+    return fail(2, "executor workspace allocation failed");
+  }
+  // QKV padding rows / unused head lanes must be finite (TMA reads them, masked after)
+  cudaMemset(e->QKV, 0, G * rows * 3 * DA * ab);
+  cudaMemset(e->AO, 0, G * rows * DA * ab);
+  *out = e;
+  return 0;
+}
+
+int flame_exec_destroy(FlameExec* e) {
+  delete e;
+  return 0;
+}
+
+int flame_exec_run(FlameExec* e, int mode, void* stream) {
+  if (!e) return fail(1, "null executor");
+  int n = 0;
+  int rc = exec_run(e, mode, static_cast<cudaStream_t>(stream), &n);
+  if (rc == 0) e->launches = n;
+  return rc;
+}
+
+int flame_exec_capture(FlameExec* e, int mode, void* stream) {
+  if (!e) return fail(1, "null executor");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  bool own = false;
+  if (s == nullptr) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    own = true;
+  }
+  // one eager run first: sets kernel attributes outside of capture
+  int rc = exec_run(e, mode, s, nullptr);
+  if (rc == 0) {
+    if (e->graph_exec) { cudaGraphExecDestroy(e->graph_exec); e->graph_exec = nullptr; }
+    if (e->graph) { cudaGraphDestroy(e->graph); e->graph = nullptr; }
+    cudaError_t err = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (err != cudaSuccess) rc = fail(2, std::string("begin capture: ") + cudaGetErrorString(err));
+    if (rc == 0) {
+      int n = 0;
+      rc = exec_run(e, mode, s, &n);
+      cudaGraph_t g = nullptr;
+      err = cudaStreamEndCapture(s, &g);
+      if (rc == 0 && err != cudaSuccess) rc = fail(2, std::string("end capture: ") + cudaGetErrorString(err));
+      if (rc == 0) {
+        e->graph = g;
+        err = cudaGraphInstantiate(&e->graph_exec, g, 0);
+        if (err != cudaSuccess) rc = fail(2, std::string("graph instantiate: ") + cudaGetErrorString(err));
+        e->graph_mode = mode;
+        e->launches = n;
+      } else if (g) {
+        cudaGraphDestroy(g);
+      }
+    }
+  }
+  if (own) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  return rc;
+}
+
+int flame_exec_replay(FlameExec* e, void* stream) {
+  if (!e || !e->graph_exec) return fail(1, "executor has no captured graph");
+  CUDA_TRY(cudaGraphLaunch(e->graph_exec, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int flame_exec_launch_count(FlameExec* e, int mode) {
+  if (!e) return -1;
+  (void)mode;
+  return e->launches;
+}
+
+void* flame_exec_workspace(FlameExec* e, const char* name) {
+  if (!e || !name) return nullptr;
+  const std::string n(name);
+  if (n == "Eh") return e->Eh;
+  if (n == "Ec") return e->Ec;
+  if (n == "qkv") return e->QKV;
+  if (n == "attn") return e->AO;
+  if (n == "fused") return e->Fz;
+  if (n == "x1") return e->X1;
+  if (n == "xout") return e->ctx->L % 2 == 1 ? e->Xa : e->Xb;
+  return nullptr;
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+// Row-wise HBM-bound kernels of the FLAME forward pass: LayerNorm (feeding the
+// projection GEMMs), the per-block sigmoid-gated fusion, the final expert dot +
+// sigmoid, and the history scatter into the block-major row space.
+#pragma once
+#include <cuda_bf16.h>
+#include "common.cuh"
+
+namespace flame {
+
+template <typename T>
+__device__ __forceinline__ void store4(T* p, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void store4<float>(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a, float b, float c,
+                                                     float d) {
+  uint2 w;
+  w.x = pack_bf16x2(a, b);
+  w.y = pack_bf16x2(c, d);
+  *reinterpret_cast<uint2*>(p) = w;
+}
+
+// LayerNorm, reference forward.py:43-47: mean, biased variance of the
+// deviations, (x - mean) / sqrt(var + 1e-5) * scale + shift.  Statistics run
+// over the first d_true columns; padded columns have scale = shift = 0 and
+// come out as 0.  One warp per row; rows of group g use gamma/beta of block g.
+template <typename TOut>
+__global__ void layer_norm_rows(const float* __restrict__ src, long long src_ld,
+                                long long src_gstride, TOut* __restrict__ out, long long out_ld,
+                                long long out_gstride, const float* __restrict__ gamma,
+                                const float* __restrict__ beta, int rows, int D, int d_true) {
+  constexpr int kMaxPerLane = 8;  // float4 chunks per lane: D <= 32*4*8 = 1024
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const int g = blockIdx.y;
+  if (warp >= rows) return;
+  const float* x = src + g * src_gstride + static_cast<long long>(warp) * src_ld;
+  float4 v[kMaxPerLane];
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxPerLane; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    v[k] = c < D ? *reinterpret_cast<const float4*>(x + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    sum += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / d_true;
+  float sq = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxPerLane; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    const float e[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float dv = e[q] - mean;
+      if (c + q < d_true) sq = fmaf(dv, dv, sq);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const float rstd = rsqrtf(sq / d_true + 1e-5f);
+  const float* ga = gamma + g * D;
+  const float* be = beta + g * D;
+  TOut* y = out + g * out_gstride + static_cast<long long>(warp) * out_ld;
+#pragma unroll
+  for (int k = 0; k < kMaxPerLane; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    if (c < D) {
+      const float4 gg = *reinterpret_cast<const float4*>(ga + c);
+      const float4 bb = *reinterpret_cast<const float4*>(be + c);
+      store4<TOut>(y + c, (v[k].x - mean) * rstd * gg.x + bb.x, (v[k].y - mean) * rstd * gg.y + bb.y,
+                   (v[k].z - mean) * rstd * gg.z + bb.z, (v[k].w - mean) * rstd * gg.w + bb.w);
+    }
+  }
+}
+
+// Gated fusion, reference forward.py:143-156:
+//   fused = sum_b sigmoid(h_b * w_b + c_b) * h_b, accumulated in block order.
+template <typename TOut>
+__global__ void gated_fusion_rows(const float* __restrict__ xc, long long x_ld, long long x_gstride,
+                                  int G, const float* __restrict__ gate_w,
+                                  const float* __restrict__ gate_b, TOut* __restrict__ out,
+                                  long long out_ld, int rows, int D) {
+  const int per_row = D / 4;
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(rows) * per_row) return;
+  const int row = static_cast<int>(idx / per_row);
+  const int c = static_cast<int>(idx % per_row) * 4;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int g = 0; g < G; ++g) {
+    const float4 h = *reinterpret_cast<const float4*>(xc + g * x_gstride + row * x_ld + c);
+    const float4 w = *reinterpret_cast<const float4*>(gate_w + g * D + c);
+    const float4 b = *reinterpret_cast<const float4*>(gate_b + g * D + c);
+    acc[0] = acc[0] + sigmoid_f(h.x * w.x + b.x) * h.x;
+    acc[1] = acc[1] + sigmoid_f(h.y * w.y + b.y) * h.y;
+    acc[2] = acc[2] + sigmoid_f(h.z * w.z + b.z) * h.z;
+    acc[3] = acc[3] + sigmoid_f(h.w * w.w + b.w) * h.w;
+  }
+  store4<TOut>(out + row * out_ld + c, acc[0], acc[1], acc[2], acc[3]);
+}
+
+// Expert output, reference forward.py:165-166: sigmoid(hidden @ w2 + b2).
+// One warp per candidate row; lane-strided dot over F in a fixed order, then a
+// fixed butterfly reduction (deterministic, batch-position invariant).
+// Padded rows (c >= C_r) are skipped; real rows go to the compact output
+// out[out_offset[r] + c][t].
+template <typename TIn>
+__global__ void expert_out_rows(const TIn* __restrict__ hidden, long long h_ld,
+                                const float* __restrict__ w2, const float* __restrict__ b2,
+                                int F, int tasks, int c_bkt, const int* __restrict__ cand_len,
+                                const int* __restrict__ out_offset, float* __restrict__ out,
+                                int rows) {
+  constexpr int kMaxTasks = 8;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (warp >= rows) return;
+  const int r = warp / c_bkt, c = warp % c_bkt;
+  if (c >= cand_len[r]) return;
+  float acc[kMaxTasks];
+#pragma unroll
+  for (int t = 0; t < kMaxTasks; ++t) acc[t] = 0.f;
+  const TIn* hrow = hidden + static_cast<long long>(warp) * h_ld;
+  for (int k = lane; k < F; k += 32) {
+    const float hv = static_cast<float>(hrow[k]);
+#pragma unroll
+    for (int t = 0; t < kMaxTasks; ++t)
+      if (t < tasks) acc[t] = fmaf(hv, w2[k * tasks + t], acc[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < kMaxTasks; ++t) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+  }
+  if (lane == 0) {
+    float* dst = out + static_cast<long long>(out_offset[r] + c) * tasks;
+    for (int t = 0; t < tasks; ++t) dst[t] = sigmoid_f(acc[t] + b2[t]);
+  }
+}
+
+// Embedding rows given by the caller ([R][H_bkt][d] history, [R][C_bkt][d]
+// candidates, fp32, width d) -> padded fp32 row space: history goes to the
+// block-major layout Eh[g][r*hb_bkt + i] = hist[r][g*hb_r + i] (the contiguous
+// Climber split of the ACTUAL length H_r, forward.py:50-62), candidates to
+// Ec[r*c_bkt + c].  Padding rows / columns are written as zeros.
+__global__ void scatter_embeddings(const float* __restrict__ hist, const float* __restrict__ cand,
+                                   int d, int D, int R, int H_bkt, int C_bkt, int G, int hb_bkt,
+                                   const int* __restrict__ hist_len, const int* __restrict__ cand_len,
+                                   float* __restrict__ Eh, float* __restrict__ Ec) {
+  // one warp per destination row; rows [0, G*R*hb_bkt) history, then R*C_bkt candidates
+  const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const long long n_hist = static_cast<long long>(G) * R * hb_bkt;
+  const long long n_cand = static_cast<long long>(R) * C_bkt;
+  if (warp >= n_hist + n_cand) return;
+  const float* src = nullptr;
+  float* dst;
+  if (warp < n_hist) {
+    const int g = static_cast<int>(warp / (static_cast<long long>(R) * hb_bkt));
+    const int rem = static_cast<int>(warp % (static_cast<long long>(R) * hb_bkt));
+    const int r = rem / hb_bkt, i = rem % hb_bkt;
+    const int hb = hist_len[r] / G;
+    if (i < hb) src = hist + (static_cast<long long>(r) * H_bkt + g * hb + i) * d;
+    dst = Eh + warp * D;
+  } else {
+    const long long row = warp - n_hist;
+    const int r = static_cast<int>(row / C_bkt), c = static_cast<int>(row % C_bkt);
+    if (c < cand_len[r]) src = cand + row * d;
+    dst = Ec + row * D;
+  }
+  for (int k = lane; k < D; k += 32) dst[k] = (src != nullptr && k < d) ? src[k] : 0.f;
+}
+
+}  // namespace flame

@@ -1,0 +1,326 @@
+"""Host side of the B200 path: device-resident model context and fixed-shape
+executors over the C ABI (include/flame_b200.h).
+
+PyTorch is used only as plumbing — device / pinned-host allocation and CUDA
+streams.  Every arithmetic step of the forward pass runs in the sm_100a
+kernels of ``_flame_b200.so``; if that library is missing the constructors
+raise instead of falling back.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import ModelConfig
+from .params import ModelParams, param_stream
+
+PRECISIONS = {"bf16": _lib.FLAME_BF16, "fp32": _lib.FLAME_FP32}
+
+
+def _next_pow2(x: int) -> int:
+    p = 1
+    while p < x:
+        p <<= 1
+    return p
+
+
+def _require_cuda(device) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the FLAME B200 path needs a CUDA device; there is no CPU fallback")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+    major, _ = torch.cuda.get_device_capability(dev)
+    if major < 10:
+        raise RuntimeError(f"device {dev} is not sm_100-class (capability major {major})")
+    return dev
+
+
+class FlameEngine:
+    """One device context: repacked weights (+ optional embedding table)."""
+
+    def __init__(self, params: ModelParams, config: ModelConfig, precision: str = "bf16",
+                 device=None) -> None:
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {tuple(PRECISIONS)}, got {precision!r}")
+        self.lib = _lib.load()
+        self.device = _require_cuda(device)
+        self.config = config
+        self.precision = precision
+        desc = _lib.FlameModelDesc(
+            config.hidden_dim, config.head_dim, config.num_blocks, config.layers_per_block,
+            config.ffn_dim, config.num_tasks, config.max_history_len, config.max_candidates,
+            config.seed)
+        stream = np.ascontiguousarray(param_stream(params), dtype=np.float64)
+        ctx = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.flame_create(ctypes.byref(desc), stream.ctypes.data, stream.size,
+                                             PRECISIONS[precision], self.device.index,
+                                             ctypes.byref(ctx)))
+        self._ctx = ctx
+        self._executors: dict[tuple, "DeviceExecutor"] = {}
+        self._lock = threading.Lock()
+        self.num_items = 0
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self._ctx is None:
+            raise RuntimeError("engine is closed")
+        return self._ctx
+
+    def set_table(self, table: np.ndarray, dtype: str = "bf16") -> None:
+        """Upload a dense embedding table (row = item id) for the id-input path."""
+        t = np.ascontiguousarray(table, dtype=np.float32)
+        if t.ndim != 2 or t.shape[1] != self.config.hidden_dim:
+            raise ValueError(f"table must be (num_items, {self.config.hidden_dim})")
+        code = {"bf16": _lib.TABLE_BF16, "fp32": _lib.TABLE_FP32}[dtype]
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.flame_set_table(self.handle, t.ctypes.data, t.shape[0], code))
+        self.num_items = t.shape[0]
+
+    def bucket(self, hist_len: int, cand_count: int) -> tuple[int, int]:
+        """(hb_bkt, c_bkt) shape bucket for one request (powers of two, capped)."""
+        cfg = self.config
+        hb = hist_len // cfg.num_blocks
+        hb_max = cfg.max_history_len // cfg.num_blocks
+        hb_bkt = min(_next_pow2(hb), hb_max) if hb > 0 else 0
+        c_bkt = max(8, _next_pow2(cand_count))
+        if c_bkt > cfg.max_candidates >= cand_count:
+            c_bkt = max(cand_count, cfg.max_candidates)
+        return hb_bkt, c_bkt
+
+    def executor(self, R: int, hb_bkt: int, c_bkt: int, *, with_ids: bool = False,
+                 cache: bool = True) -> "DeviceExecutor":
+        key = (R, hb_bkt, c_bkt, with_ids)
+        if not cache:
+            return DeviceExecutor(self, R, hb_bkt, c_bkt, with_ids=with_ids)
+        with self._lock:
+            ex = self._executors.get(key)
+            if ex is None:
+                ex = DeviceExecutor(self, R, hb_bkt, c_bkt, with_ids=with_ids)
+                self._executors[key] = ex
+            return ex
+
+    def close(self) -> None:
+        with self._lock:
+            for ex in self._executors.values():
+                ex.close()
+            self._executors.clear()
+        if self._ctx is not None:
+            self.lib.flame_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceExecutor:
+    """A fixed-shape compute slot (reference orchestrator.py:104-133 Executor):
+    caller-owned device I/O buffers + pinned host mirrors allocated once, the
+    C-side workspace, a private CUDA stream and (after ``capture``) a CUDA graph
+    of the whole forward pass.  ``score`` runs H2D -> forward -> D2H."""
+
+    def __init__(self, engine: FlameEngine, R: int, hb_bkt: int, c_bkt: int,
+                 with_ids: bool = False) -> None:
+        cfg = engine.config
+        self.engine = engine
+        self.R, self.hb_bkt, self.c_bkt = R, hb_bkt, c_bkt
+        self.H_bkt = hb_bkt * cfg.num_blocks
+        self.cap = max(self.H_bkt, c_bkt)
+        dev = engine.device
+        d, tasks = cfg.hidden_dim, cfg.num_tasks
+        self.lock = threading.Lock()
+        self.allocations = 0
+
+        def dalloc(shape, dtype):
+            self.allocations += 1
+            # never hand a null pointer to the C side for an empty (H = 0) buffer
+            t = torch.zeros(max(1, int(np.prod(shape))), dtype=dtype, device=dev)
+            return t[: int(np.prod(shape))].view(shape)
+
+        def halloc(shape, dtype):
+            self.allocations += 1
+            t = torch.zeros(max(1, int(np.prod(shape))), dtype=dtype, pin_memory=True)
+            return t[: int(np.prod(shape))].view(shape)
+
+        self.hist_emb = dalloc((R, self.H_bkt, d), torch.float32)
+        self.cand_emb = dalloc((R, c_bkt, d), torch.float32)
+        self.hist_len = dalloc((R,), torch.int32)
+        self.cand_len = dalloc((R,), torch.int32)
+        self.out_offset = dalloc((R,), torch.int32)
+        self.scores = dalloc((R * c_bkt, tasks), torch.float32)
+        self.h_meta = halloc((3, R), torch.int32)
+        self.h_scores = halloc((R * c_bkt, tasks), torch.float32)
+        self.h_hist = halloc((R, self.H_bkt, d), torch.float32)
+        self.h_cand = halloc((R, c_bkt, d), torch.float32)
+        self.with_ids = with_ids
+        if with_ids:
+            self.hist_ids = dalloc((R, self.H_bkt), torch.int64)
+            self.cand_ids = dalloc((R, c_bkt), torch.int64)
+            self.unique = dalloc((2 * R, self.cap), torch.int64)
+            self.inverse = dalloc((2 * R, self.cap), torch.int64)
+            self.n_unique = dalloc((2 * R,), torch.int32)
+            self.h_hist_ids = halloc((R, self.H_bkt), torch.int64)
+            self.h_cand_ids = halloc((R, c_bkt), torch.int64)
+        self.stream = torch.cuda.Stream(device=dev)
+        self._dummy = torch.zeros(16, dtype=torch.float32, device=dev)
+
+        def ptr(t):
+            if t is None:
+                return None
+            return t.data_ptr() if t.numel() > 0 else self._dummy.data_ptr()
+
+        io = _lib.FlameIO(
+            ptr(self.hist_emb), ptr(self.cand_emb),
+            ptr(self.hist_ids) if with_ids else None,
+            ptr(self.cand_ids) if with_ids else None,
+            ptr(self.hist_len), ptr(self.cand_len), ptr(self.out_offset), ptr(self.scores),
+            ptr(self.unique) if with_ids else None,
+            ptr(self.inverse) if with_ids else None,
+            ptr(self.n_unique) if with_ids else None)
+        ex = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _lib.check(engine.lib.flame_exec_create(engine.handle, R, hb_bkt, c_bkt, ctypes.byref(io),
+                                                    ctypes.byref(ex)))
+        self._ex = ex
+        self._graph_mode = None
+        self._finalizer = weakref.finalize(self, engine.lib.flame_exec_destroy, ex)
+        self.n_real = 0
+
+    # ------------------------------------------------------------- staging
+    def _set_meta(self, hist_lens, cand_lens) -> int:
+        R = self.R
+        if len(hist_lens) > R:
+            raise ValueError(f"{len(hist_lens)} requests exceed executor capacity {R}")
+        meta = self.h_meta.numpy()
+        meta[:] = 0
+        n = len(hist_lens)
+        meta[0, :n] = hist_lens
+        meta[1, :n] = cand_lens
+        offs = np.zeros(R, dtype=np.int64)
+        offs[1:n] = np.cumsum(np.asarray(cand_lens, dtype=np.int64))[:-1] if n > 1 else 0
+        meta[2, :n] = offs[:n]
+        self.n_real = int(np.sum(cand_lens))
+        return n
+
+    def _check_lengths(self, h: int, c: int) -> None:
+        cfg = self.engine.config
+        if h % cfg.num_blocks != 0:
+            raise ValueError(f"history length {h} is not divisible by num_blocks {cfg.num_blocks}")
+        if h > self.H_bkt:
+            raise ValueError(f"history length {h} exceeds executor capacity {self.H_bkt}")
+        if not 1 <= c <= self.c_bkt:
+            raise ValueError(f"candidate count {c} outside [1, {self.c_bkt}]")
+
+    def stage_embeddings(self, requests) -> None:
+        """requests: sequence of (history (H, d), candidates (C, d)) arrays."""
+        hl, cl = [], []
+        hh, hc = self.h_hist.numpy(), self.h_cand.numpy()
+        for r, (hist, cand) in enumerate(requests):
+            h, c = hist.shape[0], cand.shape[0]
+            self._check_lengths(h, c)
+            hh[r, :h] = hist
+            hc[r, :c] = cand
+            hl.append(h)
+            cl.append(c)
+        self._set_meta(hl, cl)
+        with torch.cuda.stream(self.stream):
+            self.hist_emb.copy_(self.h_hist, non_blocking=True)
+            self.cand_emb.copy_(self.h_cand, non_blocking=True)
+            self._upload_meta()
+
+    def stage_ids(self, requests) -> None:
+        """requests: sequence of (history ids (H,), candidate ids (C,)) int arrays."""
+        if not self.with_ids:
+            raise RuntimeError("executor was built without id buffers")
+        hl, cl = [], []
+        hh, hc = self.h_hist_ids.numpy(), self.h_cand_ids.numpy()
+        for r, (hist, cand) in enumerate(requests):
+            h, c = len(hist), len(cand)
+            self._check_lengths(h, c)
+            hh[r, :h] = hist
+            hc[r, :c] = cand
+            hl.append(h)
+            cl.append(c)
+        self._set_meta(hl, cl)
+        with torch.cuda.stream(self.stream):
+            self.hist_ids.copy_(self.h_hist_ids, non_blocking=True)
+            self.cand_ids.copy_(self.h_cand_ids, non_blocking=True)
+            self._upload_meta()
+
+    def _upload_meta(self) -> None:
+        self.hist_len.copy_(self.h_meta[0], non_blocking=True)
+        self.cand_len.copy_(self.h_meta[1], non_blocking=True)
+        self.out_offset.copy_(self.h_meta[2], non_blocking=True)
+
+    # ------------------------------------------------------------- running
+    def run(self, mode: int = _lib.INPUT_EMBEDDINGS, graph: bool = True) -> None:
+        lib = self.engine.lib
+        s = ctypes.c_void_p(self.stream.cuda_stream)
+        with torch.cuda.device(self.engine.device):
+            if graph:
+                if self._graph_mode != mode:
+                    _lib.check(lib.flame_exec_capture(self._ex, mode, s))
+                    self._graph_mode = mode
+                _lib.check(lib.flame_exec_replay(self._ex, s))
+            else:
+                _lib.check(lib.flame_exec_run(self._ex, mode, s))
+
+    def fetch_scores(self) -> np.ndarray:
+        n = self.n_real
+        with torch.cuda.stream(self.stream):
+            self.h_scores[:n].copy_(self.scores[:n], non_blocking=True)
+        self.stream.synchronize()
+        return self.h_scores[:n].numpy().astype(np.float64)
+
+    def score(self, requests, graph: bool = True) -> list[np.ndarray]:
+        """Score a batch of (history, candidates) embedding requests."""
+        with self.lock:
+            self.stage_embeddings(requests)
+            self.run(_lib.INPUT_EMBEDDINGS, graph)
+            flat = self.fetch_scores()
+        return _split_rows(flat, [c.shape[0] for _, c in requests])
+
+    def score_ids(self, requests, graph: bool = True) -> list[np.ndarray]:
+        """Score a batch of (history ids, candidate ids) requests via the PDA path."""
+        with self.lock:
+            self.stage_ids(requests)
+            self.run(_lib.INPUT_IDS, graph)
+            flat = self.fetch_scores()
+        return _split_rows(flat, [len(c) for _, c in requests])
+
+    def launch_count(self) -> int:
+        return int(self.engine.lib.flame_exec_launch_count(self._ex, 0))
+
+    def workspace(self, name: str) -> int:
+        return int(self.engine.lib.flame_exec_workspace(self._ex, name.encode()) or 0)
+
+    def read_workspace(self, name: str, shape, dtype=np.float32) -> np.ndarray:
+        """Copy an internal workspace tensor to the host (parity debugging)."""
+        self.stream.synchronize()
+        ptr = self.workspace(name)
+        if not ptr:
+            raise KeyError(name)
+        out = np.empty(shape, dtype=dtype)
+        _lib.check(self.engine.lib.flame_copy_to_host(out.ctypes.data, ptr, out.nbytes))
+        return out
+
+    def close(self) -> None:
+        if self._finalizer.alive:
+            self.stream.synchronize()
+            self._finalizer()
+
+
+def _split_rows(flat: np.ndarray, counts) -> list[np.ndarray]:
+    out, pos = [], 0
+    for c in counts:
+        out.append(flat[pos:pos + c])
+        pos += c
+    return out
