@@ -667,8 +667,6 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
   if (R < 1 || hb_bkt < 0 || c_bkt < 1) return fail(1, "bad executor shape");
   if (static_cast<long long>(hb_bkt) * c->G > c->cfg.max_history_len)
     return fail(1, "executor history capacity exceeds max_history_len");
-  if (c_bkt > c->cfg.max_candidates && c_bkt > 128)
-    return fail(1, "executor candidate capacity exceeds max_candidates");
   const int cap = flame_exec_list_capacity(c->G, hb_bkt, c_bkt);
   if (cap > kPdaMaxList) return fail(1, "id list longer than the PDA dedup kernel supports");
   CUDA_TRY(cudaSetDevice(c->device));
