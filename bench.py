@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""FLAME SUMI-ranker hot path on B200 — benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3] [--impl ours|reference]
+
+A *step* is one pass of the hot path over one batch of R synthetic requests:
+device feature assembly (PDA dedup + gather from the HBM item table) ->
+per-block LN+QKV -> SUMI attention -> O-proj -> LN2+FFN -> gated fusion ->
+expert heads, i.e. reference ``Service.resolve_embeddings`` + ``model_forward``
+(pkg/src/flameserve/service.py:97-108, model/forward.py:186-204), replayed as
+one CUDA graph.  Metric: candidates scored / s (whole job, all ranks).
+
+* ``value``  device-timed (CUDA events on the executor stream) with the ids
+  already resident in HBM; K back-to-back graph replays.  Per-step working set
+  is several GB, far larger than the 126 MB L2, so no flush is needed.
+* ``e2e``    the same metric through the public API (``DeviceExecutor.score_ids``):
+  host ids -> pinned staging -> H2D -> forward -> D2H scores -> numpy, per step.
+* ``roofline`` the dominant kernel, timed live with per-launch CUDA events in
+  an eager profiling pass; FLOPs are algorithmic.
+* ``cpu_baseline`` the numpy oracle port of the reference (oracle/) on this
+  host's cores (rank 0, N = 1 only), a bounded sample of the same workload.
+* ``--impl reference`` times that CPU reference path alone (rank 0; other
+  ranks exit without work).
+
+Multi-GPU (torchrun, one process per GPU): requests are sharded whole across
+ranks with no collective on the data path (weak scaling: R requests per rank
+per step); barrier + device sync bracket the timed region and the duration is
+the MAX over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# name: (d, dh, N_b, L, f, tasks, H, C, requests per step per GPU, description)
+WORKLOADS = {
+    "cfg1": (64, 16, 2, 1, 256, 2, 256, 64, 1024,
+             "smallest GR ranker: 2 blocks d=64 4 heads, user seq 256, 64 candidates"),
+    "cfg2": (256, 64, 4, 1, 1024, 2, 1024, 256, 128,
+             "Climber ranker: 4 blocks d=256, user seq 1024, 256 candidates/request"),
+    "cfg3": (512, 64, 8, 1, 2048, 2, 2048, 512, 64,
+             "production shape: 8 blocks d=512, user seq 2048, 512 candidates/request"),
+    "cfg5": (768, 64, 12, 1, 3072, 2, 8184, 1024, 8,
+             "long-history stress: 12 blocks d=768, user seq 8184 (=12x682), 1024 candidates"),
+}
+NUM_ITEMS = 100_000       # reference bench default universe (bench.py:78)
+WORKLOAD_SEED = 2509
+WEIGHT_SEED = 0
+STORE_SEED = 1234
+METRIC = "candidates scored/sec (1/2/4/8 B200) and p99 request latency vs CPU ref"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def zipf_sampler(num_items: int, exponent: float = 1.0):
+    """Reference bench.py:112-127 _KeySampler (Zipf over ranks, explicit CDF)."""
+    w = 1.0 / np.arange(1, num_items + 1, dtype=np.float64) ** exponent
+    cdf = np.cumsum(w / w.sum())
+    return lambda rng, n: np.searchsorted(cdf, rng.random(n)).astype(np.int64)
+
+
+def make_requests(n: int, H: int, C: int, seed: int):
+    rng = np.random.default_rng(seed)
+    sample = zipf_sampler(NUM_ITEMS)
+    return [(sample(rng, H), sample(rng, C)) for _ in range(n)]
+
+
+def model_config(name: str):
+    import paper_2509_22681_b200 as fb
+
+    d, dh, nb, L, f, tasks, H, C, *_ = WORKLOADS[name]
+    return fb.ModelConfig(d, dh, nb, L, f, tasks, H, C, seed=WEIGHT_SEED)
+
+
+def load_peaks() -> tuple[dict, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()), "measured"
+        except Exception:
+            pass
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.proc = None
+
+    def start(self) -> None:
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for row in csv.reader(io.StringIO(out)):
+            if len(row) < 7:
+                continue
+            try:
+                sm.append(float(row[0]))
+                smax.append(float(row[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, row[3:7]):
+                if v.strip().lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------- CPU oracle
+def _oracle_worker(args):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    name, reqs = args
+    sys.path.insert(0, str(ROOT))
+    import paper_2509_22681_b200 as fb
+    from oracle import flame_oracle as orc
+    from paper_2509_22681_b200.pda import item_embedding
+
+    cfg = model_config(name)
+    params = fb.init_params(cfg)
+    lat = []
+    t_all = time.perf_counter()
+    for hid, cid in reqs:
+        t0 = time.perf_counter()
+        # resolve_embeddings (service.py:97-108): unique ids -> store rows -> expand
+        rows = []
+        for ids in (hid, cid):
+            uq, inv = np.unique(ids, return_inverse=True)
+            tab = np.stack([item_embedding(STORE_SEED, int(u), 0, cfg.hidden_dim) for u in uq])
+            rows.append(tab[inv])
+        orc.model_forward(rows[0], rows[1], params, cfg)
+        lat.append(time.perf_counter() - t0)
+    return time.perf_counter() - t_all, lat
+
+
+def cpu_reference_sample(name: str, n_requests: int, procs: int, seed: int) -> dict:
+    """Time the oracle port on ``procs`` host processes (1 BLAS thread each)."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    reqs = make_requests(n_requests, WORKLOADS[name][6], WORKLOADS[name][7], seed)
+    chunks = [(name, reqs[i::procs]) for i in range(procs) if reqs[i::procs]]
+    ctx = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(len(chunks)) as pool:
+        res = pool.map(_oracle_worker, chunks)
+    wall = time.perf_counter() - t0
+    lat = sorted(x for _, l in res for x in l)
+    C = WORKLOADS[name][7]
+    return {"wall_s": wall, "busy_s": max(r[0] for r in res), "requests": n_requests,
+            "cands": n_requests * C, "lat": lat, "procs": len(chunks)}
+
+
+def nearest_rank(series, p):
+    """Reference metrics.py:11-19 nearest-rank percentile."""
+    s = sorted(series)
+    k = max(1, int(np.ceil(p * len(s))))
+    return s[k - 1]
+
+
+# ------------------------------------------------------------------- main
+REF_REQS_PER_PROC = {"cfg1": 32, "cfg2": 2, "cfg3": 1, "cfg5": 1}
+
+
+def run_reference(args, dist) -> None:
+    if dist.rank != 0:
+        return
+    name = args.workload
+    cores = len(os.sched_getaffinity(0))
+    procs = max(1, min(cores, 32))
+    per = REF_REQS_PER_PROC.get(name, 1)
+    C = WORKLOADS[name][7]
+    cpu = _cpu_name()
+    for w in range(args.warmup):
+        cpu_reference_sample(name, procs, procs, WORKLOAD_SEED + 7 + w)
+    step_s, lats = [], []
+    for k in range(args.steps):
+        r = cpu_reference_sample(name, per * procs, procs, WORKLOAD_SEED + 100 + k)
+        step_s.append(r["busy_s"])  # compute loop only: excludes worker spawn / imports
+        lats += r["lat"]
+    total = sum(step_s)
+    value = args.steps * per * procs * C / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "candidates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (Zipf ids over 100k items, seeded)",
+        "config": {"workload": name, "desc": WORKLOADS[name][9], "requests_per_step": per * procs,
+                   "candidates_per_request": C, "history_len": WORKLOADS[name][6]},
+        "p99_ms": 1000 * nearest_rank(lats, 0.99),
+        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": procs, "kind": "port",
+                         "sample": f"{per * procs} requests per step ({procs} processes x 1 BLAS thread) "
+                                   f"on {cpu}; numpy fp64 oracle port of reference "
+                                   "resolve_embeddings + model_forward"},
+        "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _cpu_name() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
+def run_ours(args, dist) -> None:
+    import torch
+
+    import paper_2509_22681_b200 as fb
+    from paper_2509_22681_b200 import _lib
+    from paper_2509_22681_b200.pda import build_item_table
+
+    name = args.workload
+    d, dh, nb, L, f, tasks, H, C, R_default, desc = WORKLOADS[name]
+    R = args.requests or R_default
+    dev = torch.device("cuda", dist.local_rank)
+    torch.cuda.set_device(dev)
+    cfg = model_config(name)
+    params = fb.init_params(cfg)
+    eng = fb.FlameEngine(params, cfg, precision="bf16", device=dist.local_rank)
+    eng.set_table(build_item_table(NUM_ITEMS, d, STORE_SEED), dtype="bf16")
+    reqs = make_requests(R, H, C, WORKLOAD_SEED + dist.rank)
+    ex = eng.executor(R, H // nb, C, with_ids=True)
+    ex.stage_ids(reqs)
+    ex.run(_lib.INPUT_IDS, graph=True)  # capture + first replay
+    ex.stream.synchronize()
+    launches = ex.launch_count()
+
+    # ---------------------------------------------------- device-timed region
+    for _ in range(args.warmup):
+        ex.run(_lib.INPUT_IDS, graph=True)
+    ex.stream.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with torch.cuda.stream(ex.stream):
+        evs[0].record(ex.stream)
+        for k in range(args.steps):
+            ex.run(_lib.INPUT_IDS, graph=True)
+            evs[k + 1].record(ex.stream)
+    ex.stream.synchronize()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dist.barrier()
+    step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    total_ms = dist.max(sum(step_ms))
+    p99_local = nearest_rank(step_ms, 0.99)
+    p99 = dist.max(p99_local)
+    cands = R * C * args.steps * dist.world_size
+    value = cands / (total_ms / 1e3)
+
+    # -------------------------------------------------------------- e2e
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        ex.score_ids(reqs)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ex.score_ids(reqs)
+    e2e_s = dist.max(time.perf_counter() - t0)
+    e2e_value = R * C * e2e_steps * dist.world_size / e2e_s
+    h2d = R * (nb * (H // nb) + C) * 8 + 3 * R * 4
+    d2h = R * C * tasks * 4
+
+    # --------------------------------------------------- roofline (live)
+    peaks, peak_src = load_peaks()
+    prof_runs = 3
+    agg: dict = {}
+    for _ in range(prof_runs):
+        for rec in ex.profile(_lib.INPUT_IDS):
+            a = agg.setdefault(rec["name"], {"ms": 0.0, "n": 0, "flops": 0.0, "bytes": 0.0})
+            a["ms"] += rec["ms"]
+            a["n"] += 1
+            a["flops"] += rec["flops"]
+            a["bytes"] += rec["bytes"]
+    step_prof_ms = sum(a["ms"] for a in agg.values()) / prof_runs
+    top = max(agg, key=lambda k: agg[k]["ms"])
+    t = agg[top]
+    avg_ms = t["ms"] / t["n"]
+    tensor = t["flops"] > 0
+    per_launch = (t["flops"] if tensor else t["bytes"]) / t["n"]
+    achieved = per_launch / (avg_ms / 1e3) / (1e12 if tensor else 1e9)
+    peak = peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]) if tensor \
+        else peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+    traffic = None
+    ncu = ROOT / "profiles" / "ncu_dram_per_launch.json"
+    if ncu.exists():
+        try:
+            traffic = json.loads(ncu.read_text()).get(name, {}).get(top)
+        except Exception:
+            traffic = None
+    kernels = {k: {"ms_per_step": round(v["ms"] / prof_runs, 4),
+                   "share": round(v["ms"] / prof_runs / step_prof_ms, 4),
+                   "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) if v["flops"] else None,
+                   "gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)}
+               for k, v in sorted(agg.items(), key=lambda kv: -kv[1]["ms"])}
+    from paper_2509_22681_b200.flops import algorithmic_flops
+
+    step_flops = algorithmic_flops(cfg, H, C) * R
+    step_tf = step_flops / (sum(step_ms) / args.steps / 1e3) / 1e12
+
+    # ------------------------------------------------------ CPU baseline
+    cpu_baseline = None
+    if dist.world_size == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        procs = max(1, min(cores, 32))
+        n_req = procs * 2 * REF_REQS_PER_PROC.get(name, 1)
+        r = cpu_reference_sample(name, n_req, procs, WORKLOAD_SEED + 99)
+        cpu_baseline = {"value": r["cands"] / r["busy_s"], "unit": "candidates/s", "cores": r["procs"],
+                        "kind": "port",
+                        "sample": f"{n_req} requests of {name} on {r['procs']} processes x 1 BLAS thread "
+                                  f"({_cpu_name()}), numpy fp64 oracle port of reference "
+                                  f"resolve_embeddings + model_forward; compute {r['busy_s']:.1f}s; "
+                                  f"p99 {1000 * nearest_rank(r['lat'], 0.99):.0f} ms"}
+
+    if dist.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": dist.world_size,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic: Zipf(1.0) item ids over 100k items (reference _KeySampler), "
+                    "store embeddings item_embedding(seed 1234), random-init weights init_params(seed 0)",
+            "config": {"workload": name, "desc": desc, "requests_per_step_per_gpu": R,
+                       "candidates_per_request": C, "history_len": H, "num_blocks": nb,
+                       "hidden_dim": d, "layers_per_block": L, "ffn_dim": f,
+                       "parallelism": f"request-sharded dp{dist.world_size}, no collective",
+                       "l2": "per-step working set (activations, several GB) >> 126 MB L2; no flush",
+                       "input": "item ids resident in HBM; PDA gather from bf16 HBM table"},
+            "p99_ms": p99,
+            "latency_note": "a request completes when its step's graph replay completes; "
+                            "p99 over steps (nearest rank), max over ranks",
+            "step_tflops": round(step_tf, 1),
+            "e2e": {"value": e2e_value, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "path": "DeviceExecutor.score_ids: numpy ids -> pinned -> H2D -> graph -> D2H -> numpy"},
+            "gpu_launches": launches * args.steps,
+            "launches_per_step": launches,
+            "roofline": {"bound": "tensor" if tensor else "hbm", "kernel": top,
+                         "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic,
+                         "peak_source": f"{peak_src} ({'bf16_tflops_sustained' if tensor else 'hbm_gbs'})",
+                         "per_launch": per_launch, "avg_launch_ms": avg_ms},
+            "kernels": kernels,
+            "clocks": clk,
+            "cpu_baseline": cpu_baseline,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--requests", type=int, default=0, help="requests per step per GPU (0 = default)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    from paper_2509_22681_b200.sharding import Dist
+
+    dist = Dist(backend="gloo" if args.impl == "reference" else None)
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

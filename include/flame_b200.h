@@ -94,6 +94,13 @@ int flame_exec_destroy(FlameExec* ex);
 int flame_exec_run(FlameExec* ex, int input_mode, void* stream);
 int flame_exec_capture(FlameExec* ex, int input_mode, void* stream);
 int flame_exec_replay(FlameExec* ex, void* stream);
+/* Eager run with a CUDA event recorded on `stream` before every launch.
+ * Fills, per launch i < max_launches: ms[i] (device duration), names[64*i]
+ * (NUL-terminated kernel role), flops[i] / bytes[i] (algorithmic FLOPs and
+ * bytes of that launch).  Returns the number of launches (>= 0) or
+ * -status on failure.  Any output pointer may be NULL. */
+int flame_exec_profile(FlameExec* ex, int input_mode, void* stream, int max_launches, float* ms,
+                       char* names, double* flops, double* bytes);
 /* Number of kernel launches one run issues (for the bench's gpu_launches). */
 int flame_exec_launch_count(FlameExec* ex, int input_mode);
 /* Device pointer of an internal workspace tensor, for parity debugging:

@@ -21,6 +21,7 @@ EXPORTED = (
     "flame_create", "flame_create_flmp", "flame_destroy", "flame_set_table",
     "flame_exec_list_capacity", "flame_exec_create", "flame_exec_destroy", "flame_exec_run",
     "flame_exec_capture", "flame_exec_replay", "flame_exec_launch_count", "flame_exec_workspace",
+    "flame_exec_profile",
     "flame_last_error", "flame_device_sm_count", "flame_copy_to_host",
 )
 
@@ -66,6 +67,7 @@ def load() -> ctypes.CDLL:
             "flame_exec_capture": (I, [P, I, P]),
             "flame_exec_replay": (I, [P, P]),
             "flame_exec_launch_count": (I, [P, I]),
+            "flame_exec_profile": (I, [P, I, P, I, P, P, P, P]),
             "flame_exec_workspace": (P, [P, ctypes.c_char_p]),
             "flame_last_error": (ctypes.c_char_p, []),
             "flame_device_sm_count": (I, [I]),

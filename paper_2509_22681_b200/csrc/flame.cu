@@ -314,14 +314,35 @@ int validate_desc(const FlameModelDesc& m) {
 // --------------------------------------------------------------- pipeline
 namespace {
 
+// Per-launch profiler: an event is recorded on the launching stream before
+// every launch (and once at the end); consecutive differences are the launch
+// durations.  Each launch also carries its algorithmic FLOPs and bytes.
+struct Prof {
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::string> names;
+  std::vector<double> flops, bytes;
+};
+
 template <typename Act>
 struct Pipe {
   FlameExec* e;
   FlameCtx* c;
   cudaStream_t s;
   int launches = 0;
+  Prof* prof = nullptr;
 
   Act* act(void* p) { return static_cast<Act*>(p); }
+
+  void mark(const char* name, double flops, double bytes) {
+    if (!prof) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, s);
+    prof->ev.push_back(ev);
+    prof->names.emplace_back(name);
+    prof->flops.push_back(flops);
+    prof->bytes.push_back(bytes);
+  }
 
   int check() {
     cudaError_t err = cudaGetLastError();
@@ -330,6 +351,7 @@ struct Pipe {
     return 0;
   }
 
+  const char* gemm_name = "gemm";
   int gemm(const Act* A, long long lda, long long a_gstride, int a_shared, const Act* W, long long ldw,
            long long w_gstride, int M, int N, int K, int G, void* out, long long out_ld,
            long long out_gstride, int out_col0, const float* bias, long long bias_gstride,
@@ -340,6 +362,13 @@ struct Pipe {
     ep.resid = resid; ep.resid_ld = resid_ld; ep.resid_gstride = resid_gstride;
     ep.M = M; ep.N = N;
     if (M <= 0) return 0;
+    {
+      const double ab = sizeof(Act);
+      const double ob = (epi & EPI_OUT_F32) || !std::is_same<Act, __nv_bfloat16>::value ? 4.0 : 2.0;
+      const double byts = static_cast<double>(G) * (static_cast<double>(M) * K * ab + static_cast<double>(N) * K * ab +
+                                                    static_cast<double>(M) * N * (ob + ((epi & EPI_RESID) ? 4.0 : 0.0)));
+      mark(gemm_name, 2.0 * G * static_cast<double>(M) * N * K, byts);
+    }
     if constexpr (std::is_same<Act, __nv_bfloat16>::value) {
       GemmProblem p{};
       p.A = A; p.lda = lda; p.a_gstride = a_gstride; p.a_shared = a_shared;
@@ -373,6 +402,7 @@ struct Pipe {
     if (rows <= 0) return 0;
     const int threads = 256;
     dim3 grid(static_cast<unsigned>((rows * 32 + threads - 1) / threads), c->G);
+    mark("layer_norm", 0.0, static_cast<double>(c->G) * rows * c->D * (4.0 + sizeof(Act)));
     layer_norm_rows<Act><<<grid, threads, 0, s>>>(src, src_ld, src_gstride, out, out_ld, out_gstride,
                                                   gamma, beta, static_cast<int>(rows), c->D, c->d);
     return check();
@@ -382,6 +412,15 @@ struct Pipe {
     const int tiles = hist ? (e->hb_bkt + 127) / 128 : (e->c_bkt + 127) / 128;
     if (tiles == 0 || e->R == 0) return 0;
     dim3 grid(tiles, c->nh, c->G * e->R);
+    {
+      // algorithmic: 4*dh per allowed (row, key) pair; rows = real rows of the bucket shape
+      const double hb = e->hb_bkt, cc = e->c_bkt;
+      const double pairs = hist ? hb * (hb + 1) / 2 : cc * (hb + 1);
+      const double fl = 4.0 * 64 * c->nh * pairs * c->G * e->R;
+      const double rows = hist ? hb : cc;
+      const double by = static_cast<double>(c->G) * e->R * c->nh * 64 * sizeof(Act) * (3.0 * rows + 2.0 * hb + rows);
+      mark(hist ? "attention_hist" : "attention_sumi", fl, by);
+    }
     if constexpr (std::is_same<Act, __nv_bfloat16>::value) {
       AttnArgs a{};
       a.qkv = act(e->QKV); a.out = act(e->AO);
@@ -423,6 +462,7 @@ struct Pipe {
       if (!e->io.hist_emb || !e->io.cand_emb) return fail(1, "embedding inputs not bound");
       const long long warps = static_cast<long long>(c->G) * e->Rh + e->Rc;
       const int threads = 256;
+      mark("scatter_embeddings", 0.0, static_cast<double>(warps) * (c->d + c->D) * 4.0);
       scatter_embeddings<<<static_cast<unsigned>((warps * 32 + threads - 1) / threads), threads, 0, s>>>(
           e->io.hist_emb, e->io.cand_emb, c->d, c->D, e->R, e->H_bkt, e->c_bkt, c->G, e->hb_bkt,
           e->io.hist_len, e->io.cand_len, e->Eh, e->Ec);
@@ -446,6 +486,7 @@ struct Pipe {
       cudaFuncSetAttribute(pda_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       smem_set = smem;
     }
+    mark("pda_dedup", 0.0, static_cast<double>(e->R) * (e->H_bkt + e->c_bkt) * (8.0 + 8.0 + 8.0 + 8.0));
     pda_dedup<<<2 * e->R, kPdaThreads, smem, s>>>(l);
     if (int rc = check()) return rc;
     {
@@ -457,6 +498,9 @@ struct Pipe {
       const int max_bx = (e->cap + 7) / 8;
       if (bx > max_bx) bx = max_bx < 1 ? 1 : max_bx;
       dim3 grid(bx, 2 * e->R);
+      // rows out (fp32) + table rows read (upper bound: one per position)
+      mark("pda_gather", 0.0, static_cast<double>(e->R) * (e->H_bkt + e->c_bkt) * c->D *
+                                  (4.0 + (c->table_dtype == FLAME_TABLE_BF16 ? 2.0 : 4.0)));
       if (c->table_dtype == FLAME_TABLE_BF16)
         pda_gather<__nv_bfloat16><<<grid, 256, 0, s>>>(g);
       else
@@ -492,21 +536,26 @@ struct Pipe {
       // projections (forward.py:112-114 last layer: history rows K,V only; :121-123 others)
       const Act* Wqkv = act(w.wqkv);
       if (last) {
+        gemm_name = "gemm_kv_hist";
         if (int rc = gemm(Y, D, gD, 0, Wqkv + static_cast<long long>(DA) * D, D, 3LL * DA * D, Rh, 2 * DA, D, G,
                           QKV, 3LL * DA, gQKV, DA, nullptr, 0, nullptr, 0, 0, 0)) return rc;
       } else {
+        gemm_name = "gemm_qkv_hist";
         if (int rc = gemm(Y, D, gD, 0, Wqkv, D, 3LL * DA * D, Rh, 3 * DA, D, G, QKV, 3LL * DA, gQKV, 0,
                           nullptr, 0, nullptr, 0, 0, 0)) return rc;
       }
+      gemm_name = "gemm_qkv_cand";
       if (int rc = gemm(Y + Rh * D, D, gD, 0, Wqkv, D, 3LL * DA * D, Rc, 3 * DA, D, G, QKV + Rh * 3LL * DA,
                         3LL * DA, gQKV, 0, nullptr, 0, nullptr, 0, 0, 0)) return rc;
       // SUMI attention (attention.py:118-146; :149-178 for non-final layers)
       if (int rc = attention(false)) return rc;
       if (!last) { if (int rc = attention(true)) return rc; }
       // O-projection + residual (forward.py:116 / :135)
+      gemm_name = "gemm_oproj_cand";
       if (int rc = gemm(AO + Rh * DA, DA, gA, 0, act(w.wo), DA, static_cast<long long>(D) * DA, Rc, D, DA, G,
                         e->X1 + Rh * D, D, gD, 0, nullptr, 0, src_c, D, src_c_g, EPI_RESID | EPI_OUT_F32)) return rc;
       if (!last) {
+        gemm_name = "gemm_oproj_hist";
         if (int rc = gemm(AO, DA, gA, 0, act(w.wo), DA, static_cast<long long>(D) * DA, Rh, D, DA, G, e->X1, D, gD, 0,
                           nullptr, 0, src_h, D, src_h_g, EPI_RESID | EPI_OUT_F32)) return rc;
       }
@@ -514,8 +563,10 @@ struct Pipe {
       const long long r0 = last ? Rh : 0;  // first row of the range that continues
       const long long nr = last ? Rc : rows;
       if (int rc = layer_norm(e->X1 + r0 * D, D, gD, Y + r0 * D, D, gD, w.ln2_g, w.ln2_b, nr)) return rc;
+      gemm_name = "gemm_ffn_w1";
       if (int rc = gemm(Y + r0 * D, D, gD, 0, act(w.w1), D, static_cast<long long>(F) * D, static_cast<int>(nr), F, D, G,
                         Hf + r0 * F, F, gF, 0, w.b1, F, nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
+      gemm_name = "gemm_ffn_w2";
       if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F, G,
                         Xnext + r0 * D, D, gD, 0, w.b2, D, e->X1 + r0 * D, D, gD,
                         EPI_BIAS | EPI_RESID | EPI_OUT_F32)) return rc;
@@ -524,15 +575,18 @@ struct Pipe {
     // gated fusion over blocks (forward.py:143-156)
     {
       const long long n = Rc * (D / 4);
+      mark("gated_fusion", 0.0, static_cast<double>(Rc) * D * (4.0 * G + sizeof(Act)));
       gated_fusion_rows<Act><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
           Xcur + Rh * D, D, gD, G, c->gate_w, c->gate_b, act(e->Fz), D, static_cast<int>(Rc), D);
       if (int rc = check()) return rc;
     }
     // expert heads (forward.py:159-166)
+    gemm_name = "gemm_expert_w1";
     if (int rc = gemm(act(e->Fz), D, 0, 1, act(c->we1), D, 0, static_cast<int>(Rc), F, D, 1, e->He, F, 0, 0, c->be1, 0,
                       nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
     {
       const long long threads = Rc * 32;
+      mark("expert_out", 2.0 * Rc * F * c->tasks, static_cast<double>(Rc) * F * sizeof(Act));
       expert_out_rows<Act><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
           act(e->He), F, c->we2, c->be2, F, c->tasks, e->c_bkt, e->io.cand_len, e->io.out_offset,
           e->io.scores, static_cast<int>(Rc));
@@ -542,7 +596,7 @@ struct Pipe {
   }
 };
 
-int exec_run(FlameExec* e, int mode, cudaStream_t s, int* launches) {
+int exec_run(FlameExec* e, int mode, cudaStream_t s, int* launches, Prof* prof = nullptr) {
   if (mode < 0 || mode > 2) return fail(1, "bad input mode");
   if (mode != FLAME_INPUT_GATHER_ONLY && !e->io.scores) return fail(1, "scores buffer not bound");
   if (!e->io.hist_len || !e->io.cand_len || !e->io.out_offset) return fail(1, "length buffers not bound");
@@ -550,11 +604,15 @@ int exec_run(FlameExec* e, int mode, cudaStream_t s, int* launches) {
   int n = 0;
   if (e->ctx->precision == FLAME_BF16) {
     Pipe<__nv_bfloat16> p{e, e->ctx, s};
+    p.prof = prof;
     rc = p.run(mode);
+    p.mark("end", 0.0, 0.0);
     n = p.launches;
   } else {
     Pipe<float> p{e, e->ctx, s};
+    p.prof = prof;
     rc = p.run(mode);
+    p.mark("end", 0.0, 0.0);
     n = p.launches;
   }
   if (launches) *launches = n;
@@ -768,6 +826,33 @@ int flame_exec_replay(FlameExec* e, void* stream) {
   if (!e || !e->graph_exec) return fail(1, "executor has no captured graph");
   CUDA_TRY(cudaGraphLaunch(e->graph_exec, static_cast<cudaStream_t>(stream)));
   return 0;
+}
+
+int flame_exec_profile(FlameExec* e, int mode, void* stream, int max_launches, float* ms,
+                       char* names, double* flops, double* bytes) {
+  if (!e || max_launches < 1) return fail(1, "bad profile arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Prof prof;
+  int rc = exec_run(e, mode, s, nullptr, &prof);
+  cudaError_t err = cudaStreamSynchronize(s);
+  int n = static_cast<int>(prof.ev.size()) - 1;  // last event is the end marker
+  if (rc == 0 && err != cudaSuccess) rc = fail(2, std::string("profile: ") + cudaGetErrorString(err));
+  if (rc == 0) {
+    if (n > max_launches) n = max_launches;
+    for (int i = 0; i < n; ++i) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, prof.ev[i], prof.ev[i + 1]);
+      if (ms) ms[i] = t;
+      if (flops) flops[i] = prof.flops[i];
+      if (bytes) bytes[i] = prof.bytes[i];
+      if (names) {
+        std::strncpy(names + 64 * i, prof.names[i].c_str(), 63);
+        names[64 * i + 63] = 0;
+      }
+    }
+  }
+  for (cudaEvent_t ev : prof.ev) cudaEventDestroy(ev);
+  return rc == 0 ? n : -rc;
 }
 
 int flame_exec_launch_count(FlameExec* e, int mode) {

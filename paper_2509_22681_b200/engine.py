@@ -296,6 +296,23 @@ class DeviceExecutor:
             flat = self.fetch_scores()
         return _split_rows(flat, [len(c) for _, c in requests])
 
+    def profile(self, mode: int = _lib.INPUT_EMBEDDINGS, max_launches: int = 256) -> list[dict]:
+        """One eager run with per-launch CUDA events on this executor's stream:
+        [{name, ms, flops, bytes}] in launch order."""
+        ms = np.zeros(max_launches, np.float32)
+        names = ctypes.create_string_buffer(64 * max_launches)
+        flops = np.zeros(max_launches, np.float64)
+        byts = np.zeros(max_launches, np.float64)
+        with torch.cuda.device(self.engine.device):
+            n = self.engine.lib.flame_exec_profile(
+                self._ex, mode, ctypes.c_void_p(self.stream.cuda_stream), max_launches,
+                ms.ctypes.data, names, flops.ctypes.data, byts.ctypes.data)
+        if n < 0:
+            _lib.check(-n)
+        raw = names.raw
+        return [{"name": raw[64 * i:64 * i + 64].split(b"\0")[0].decode(), "ms": float(ms[i]),
+                 "flops": float(flops[i]), "bytes": float(byts[i])} for i in range(n)]
+
     def launch_count(self) -> int:
         return int(self.engine.lib.flame_exec_launch_count(self._ex, 0))
 

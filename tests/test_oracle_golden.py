@@ -54,3 +54,12 @@ def test_algorithmic_flops_survey_values():
     assert abs(orc.algorithmic_flops(cfg3, 2048, 512) / 3.115e10 - 1) < 2e-3
     cfg2 = fb.ModelConfig(256, 64, 4, 1, 1024, 2, 1024, 256)
     assert abs(orc.algorithmic_flops(cfg2, 1024, 256) / 2.28e9 - 1) < 5e-3
+
+
+def test_package_flop_formula_matches_oracle_formula():
+    import paper_2509_22681_b200 as fb
+    from paper_2509_22681_b200.flops import algorithmic_flops
+
+    for dims, H, C in [((64, 16, 2, 2, 256, 2, 256, 64), 256, 64), ((512, 64, 8, 1, 2048, 2, 2048, 512), 2048, 512)]:
+        cfg = fb.ModelConfig(*dims)
+        assert algorithmic_flops(cfg, H, C) == orc.algorithmic_flops(cfg, H, C)
