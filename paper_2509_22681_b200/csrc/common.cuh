@@ -29,61 +29,29 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <typename GemmEpilogueT>
-__device__ __forceinline__ void store_row_segment_bf16(const GemmEpilogueT& ep, int g, int row,
-                                                       int col0, const float* v, int n) {
-  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep.out) + g * ep.out_gstride +
-                       static_cast<long long>(row) * ep.out_ld + ep.out_col0 + col0;
-  if (n == 32 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 w;
-      w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-      w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-      w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-      w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-      reinterpret_cast<uint4*>(out)[q] = w;
-    }
-  } else {
-    for (int j = 0; j < n; ++j) out[j] = __float2bfloat16_rn(v[j]);
-  }
-}
-
-template <typename GemmEpilogueT>
-__device__ __forceinline__ void store_row_segment_f32(const GemmEpilogueT& ep, int g, int row,
-                                                      int col0, const float* v, int n) {
-  float* out = reinterpret_cast<float*>(ep.out) + g * ep.out_gstride +
-               static_cast<long long>(row) * ep.out_ld + ep.out_col0 + col0;
-  if (n == 32 && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      reinterpret_cast<float4*>(out)[q] =
-          make_float4(v[q * 4 + 0], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
-  } else {
-    for (int j = 0; j < n; ++j) out[j] = v[j];
-  }
-}
-
-// Apply bias -> GELU -> residual (that order matches the reference:
-// gelu(y@w1+b1) and x + (...)@w2 + b2) to NV consecutive columns of one row.
-template <int EPI, int NV, bool kFastMath = true, typename GemmEpilogueT>
-__device__ __forceinline__ void epilogue_apply(float* v, const GemmEpilogueT& ep, int g, int row,
-                                               int col0) {
+// Fused epilogue math on NV consecutive columns of one row, kept in registers
+// (every index is a compile-time constant): bias -> GELU -> residual, the order
+// of the reference (gelu(y@w1+b1), x + (...)@w2 + b2).  Columns >= ep.N are
+// left untouched (the store clips them).
+template <int EPI, int NV, bool kFastMath, typename GemmEpilogueT>
+__device__ __forceinline__ void epilogue_math(float (&v)[NV], const GemmEpilogueT& ep, int g,
+                                              int row, int col0) {
   constexpr bool kBias = (EPI & 1) != 0;
   constexpr bool kGelu = (EPI & 2) != 0;
   constexpr bool kResid = (EPI & 4) != 0;
-  constexpr bool kF32 = (EPI & 8) != 0;
-  const int n = min(NV, ep.N - col0);
+  const bool full = col0 + NV <= ep.N;
   if constexpr (kBias) {
     const float* b = ep.bias + g * ep.bias_gstride + col0;
-    if (n == NV) {
+    if (full) {
 #pragma unroll
       for (int j = 0; j < NV; j += 4) {
-        const float4 bb = *reinterpret_cast<const float4*>(b + j);
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(b + j));
         v[j] += bb.x; v[j + 1] += bb.y; v[j + 2] += bb.z; v[j + 3] += bb.w;
       }
     } else {
-      for (int j = 0; j < n; ++j) v[j] += b[j];
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (col0 + j < ep.N) v[j] += b[j];
     }
   }
   if constexpr (kGelu) {
@@ -92,20 +60,69 @@ __device__ __forceinline__ void epilogue_apply(float* v, const GemmEpilogueT& ep
   }
   if constexpr (kResid) {
     const float* rp = ep.resid + g * ep.resid_gstride + static_cast<long long>(row) * ep.resid_ld + col0;
-    if (n == NV) {
+    if (full) {
 #pragma unroll
       for (int j = 0; j < NV; j += 4) {
         const float4 rr = *reinterpret_cast<const float4*>(rp + j);
         v[j] += rr.x; v[j + 1] += rr.y; v[j + 2] += rr.z; v[j + 3] += rr.w;
       }
     } else {
-      for (int j = 0; j < n; ++j) v[j] += rp[j];
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (col0 + j < ep.N) v[j] += rp[j];
     }
   }
+}
+
+// Direct (non-TMA) store of NV columns of one row, predicated on ep.N.
+template <int EPI, int NV, typename GemmEpilogueT>
+__device__ __forceinline__ void epilogue_store_direct(const float (&v)[NV], const GemmEpilogueT& ep,
+                                                      int g, int row, int col0) {
+  constexpr bool kF32 = (EPI & 8) != 0;
+  const long long off = g * ep.out_gstride + static_cast<long long>(row) * ep.out_ld + ep.out_col0 + col0;
   if constexpr (kF32) {
-    store_row_segment_f32(ep, g, row, col0, v, n);
+    float* out = reinterpret_cast<float*>(ep.out) + off;
+    if (col0 + NV <= ep.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < NV; j += 4)
+        *reinterpret_cast<float4*>(out + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (col0 + j < ep.N) out[j] = v[j];
+    }
   } else {
-    store_row_segment_bf16(ep, g, row, col0, v, n);
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep.out) + off;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+      if (col0 + j < ep.N) out[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+// Write 32 columns of one row into a 32x32 TMA staging box (row = lane).
+// bf16: 64-byte rows, SWIZZLE_64B (16-byte chunk c -> c ^ ((r >> 1) & 3));
+// fp32: 128-byte rows, SWIZZLE_128B (chunk c -> c ^ (r & 7)).  Both patterns
+// are bank-conflict free for a warp writing one row per lane.
+template <bool kF32>
+__device__ __forceinline__ void stage_row32(uint8_t* box, int r, const float (&v)[32]) {
+  if constexpr (kF32) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cc = c ^ (r & 7);
+      *reinterpret_cast<float4*>(box + r * 128 + cc * 16) =
+          make_float4(v[c * 4 + 0], v[c * 4 + 1], v[c * 4 + 2], v[c * 4 + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int cc = c ^ ((r >> 1) & 3);
+      uint4 w;
+      w.x = pack_bf16x2(v[c * 8 + 0], v[c * 8 + 1]);
+      w.y = pack_bf16x2(v[c * 8 + 2], v[c * 8 + 3]);
+      w.z = pack_bf16x2(v[c * 8 + 4], v[c * 8 + 5]);
+      w.w = pack_bf16x2(v[c * 8 + 6], v[c * 8 + 7]);
+      *reinterpret_cast<uint4*>(box + r * 64 + cc * 16) = w;
+    }
   }
 }
 

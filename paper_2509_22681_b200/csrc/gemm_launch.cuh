@@ -35,6 +35,11 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
     return cudaErrorInvalidValue;
   if (!make_tmap_bf16_3d(&tb, p.W, p.K, p.N, p.G, p.ldw * 2, p.w_gstride * 2, gemm::BK, BN))
     return cudaErrorInvalidValue;
+  CUtensorMap to;
+  constexpr int ob = (EPI & EPI_OUT_F32) ? 4 : 2;
+  if (!make_tmap_out_3d(&to, p.ep.out, ob, static_cast<uint64_t>(p.ep.out_col0) + p.N, p.M, p.G,
+                        p.ep.out_ld * ob, p.ep.out_gstride * ob))
+    return cudaErrorInvalidValue;
   const int m_tiles = (p.M + gemm::BM - 1) / gemm::BM;
   const int n_tiles = (p.N + BN - 1) / BN;
   const int total = p.G * m_tiles * n_tiles;
@@ -43,7 +48,7 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   ep.M = p.M;
   ep.N = p.N;
   gemm_bf16_tcgen05<BN, EPI><<<grid, gemm::kThreads, C::kSmemBytes, s>>>(
-      ta, tb, p.K / gemm::BK, m_tiles, n_tiles, p.G, p.a_shared, ep);
+      ta, tb, to, p.K / gemm::BK, m_tiles, n_tiles, p.G, p.a_shared, ep);
   return cudaGetLastError();
 }
 

@@ -9,7 +9,9 @@
 //   warp 0      : TMA producer (A + W tiles into a kStages-deep smem ring)
 //   warp 1      : MMA issuer (one thread issues tcgen05.mma, commits to mbarriers)
 //   warp 2      : TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
-//   warps 4..7  : epilogue (tcgen05.ld -> bias / tanh-GELU / fp32 residual -> store)
+//   warps 4..11 : epilogue — two warps per TMEM lane quadrant, each taking every
+//                 other 32-column chunk: tcgen05.ld -> bias / tanh-GELU / fp32
+//                 residual in registers -> swizzled smem box -> TMA bulk store
 // The epilogue of tile i overlaps the MMAs of tile i+1 through the second
 // accumulator buffer.  The K loop order is fixed per row, so a row's result is
 // independent of which tile / batch position it lands in (batch invariance:
@@ -44,7 +46,9 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kBoxBytes = 32 * 32 * 4;  // one 32x32 staging box per epilogue warp (fp32 worst case)
 
 template <int BN>
 struct Cfg {
@@ -53,7 +57,8 @@ struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + kEpiWarps * kBoxBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 }  // namespace gemm
@@ -61,7 +66,7 @@ struct Cfg {
 template <int BN, int EPI>
 __global__ void __launch_bounds__(gemm::kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      int num_k_blocks, int m_tiles, int n_tiles, int groups, int a_shared,
+                      const __grid_constant__ CUtensorMap tmO, int num_k_blocks, int m_tiles, int n_tiles, int groups, int a_shared,
                       GemmEpilogue ep) {
   using C = gemm::Cfg<BN>;
   constexpr int kStages = C::kStages;
@@ -71,7 +76,8 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
   uint8_t* smem = smem_raw + pad;
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * C::kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+  uint8_t* smem_box = smem + kStages * C::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_box + gemm::kEpiWarps * gemm::kBoxBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tmem_full = bars + 2 * kStages;
@@ -84,13 +90,14 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
+    ptx::tma_prefetch_desc(&tmO);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tmem_full[s], 1);
-      ptx::mbar_init(&tmem_empty[s], 4);
+      ptx::mbar_init(&tmem_empty[s], gemm::kEpiWarps);
     }
     ptx::fence_barrier_init();
   }
@@ -151,7 +158,11 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
     }
   } else if (warp >= 4) {
     // ----------------------------------------------------------- epilogue
-    const int wq = warp & 3;  // TMEM lane quadrant this warp may access
+    constexpr bool kF32 = (EPI & EPI_OUT_F32) != 0;
+    const int ew = warp - 4;
+    const int wq = warp & 3;    // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;   // which interleaved half of the 32-column chunks
+    uint8_t* box = smem_box + ew * gemm::kBoxBytes;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
@@ -160,26 +171,38 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
       const int g = tile / (n_tiles * m_tiles);
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
-      const int row = m_blk * gemm::BM + wq * 32 + lane;
-      const bool row_ok = row < ep.M;
+      const int row0 = m_blk * gemm::BM + wq * 32;
+      // rows past M are clipped by the TMA store; clamp their residual reads
+      const int row = min(row0 + lane, ep.M - 1);
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
         ptx::tmem_ld_wait();
         const int col0 = n_blk * BN + c * 32;
-        if (!row_ok || col0 >= ep.N) continue;
+        if (col0 >= ep.N) continue;  // warp-uniform
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        epilogue_apply<EPI, 32>(v, ep, g, row, col0);
+        epilogue_math<EPI, 32, true>(v, ep, g, row, col0);
+        if (lane == 0) ptx::tma_store_wait_read<0>();  // staging box free again
+        __syncwarp();
+        stage_row32<kF32>(box, lane, v);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_3d(&tmO, box, ep.out_col0 + col0, row0, g);
+          ptx::tma_store_commit();
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) ptx::tma_store_wait<0>();
+    __syncwarp();
   }
 
   ptx::tc_fence_before();

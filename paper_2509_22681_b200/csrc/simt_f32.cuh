@@ -56,7 +56,10 @@ __global__ void __launch_bounds__(256) gemm_f32_simt(const float* __restrict__ A
   for (int i = 0; i < 8; ++i) {
     const int row = m0 + ty * 8 + i;
     const int col0 = n0 + tx * 8;
-    if (row < M && col0 < N) epilogue_apply<EPI, 8, false>(acc[i], ep, g, row, col0);
+    if (row < M && col0 < N) {
+      epilogue_math<EPI, 8, false>(acc[i], ep, g, row, col0);
+      epilogue_store_direct<EPI, 8>(acc[i], ep, g, row, col0);
+    }
   }
 }
 
