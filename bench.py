@@ -256,7 +256,7 @@ def run_ours(args, dist) -> None:
     cfg = model_config(name)
     params = fb.init_params(cfg)
     eng = fb.FlameEngine(params, cfg, precision="bf16", device=dist.local_rank)
-    eng.set_table(build_item_table(NUM_ITEMS, d, STORE_SEED), dtype="bf16")
+    eng.set_table(build_item_table(NUM_ITEMS, d, STORE_SEED), dtype="fp32")
     reqs = make_requests(R, H, C, WORKLOAD_SEED + dist.rank)
     ex = eng.executor(R, H // nb, C, with_ids=True)
     ex.stage_ids(reqs)
@@ -367,7 +367,7 @@ def run_ours(args, dist) -> None:
                        "hidden_dim": d, "layers_per_block": L, "ffn_dim": f,
                        "parallelism": f"request-sharded dp{dist.world_size}, no collective",
                        "l2": "per-step working set (activations, several GB) >> 126 MB L2; no flush",
-                       "input": "item ids resident in HBM; PDA gather from bf16 HBM table"},
+                       "input": "item ids resident in HBM; PDA gather from the fp32 HBM item table"},
             "p99_ms": p99,
             "latency_note": "a request completes when its step's graph replay completes; "
                             "p99 over steps (nearest rank), max over ranks",

@@ -43,6 +43,8 @@ FORWARD_CASES = [
     ("l3_nb4", (32, 8, 4, 3, 96, 3, 128, 64, 9), 64, 33, True),
     ("cfg2", (256, 64, 4, 1, 1024, 2, 1024, 256, 0), 1024, 256, False),
     ("cfg3", (512, 64, 8, 1, 2048, 2, 2048, 512, 0), 2048, 512, False),
+    ("long_hist_l2", (128, 64, 2, 2, 256, 2, 1200, 700, 12), 1200, 700, False),
+    ("cfg5", (768, 64, 12, 1, 3072, 2, 8184, 1024, 0), 8184, 1024, False),
 ]
 
 

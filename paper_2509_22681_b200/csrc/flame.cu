@@ -255,10 +255,27 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
     if (!need(d)) return fail(1, "weights too short (gate_bias)");
     for (int i = 0; i < d; ++i) gate_b[static_cast<size_t>(b) * D + i] = static_cast<float>(a[i]);
   }
-  std::vector<T> we1(static_cast<size_t>(F) * D, cvt<T>(0.0));
+  // expert W1: bf16 mode stores the 3-term split [W_hi | W_lo | W_hi] along K
+  // (the expert head dominates the bf16 error budget: DESIGN.md §5)
+  constexpr bool kSplit = std::is_same<T, __nv_bfloat16>::value;
+  const int DK = kSplit ? 3 * D : D;
+  std::vector<T> we1(static_cast<size_t>(F) * DK, cvt<T>(0.0));
   std::vector<float> be1(F, 0.f), we2(static_cast<size_t>(F) * tasks, 0.f), be2(tasks, 0.f);
   if (!need(static_cast<long long>(d) * f)) return fail(1, "weights too short (expert_w1)");
-  pack_transposed(we1, 0, F, D, a, d, f, id_f, id_d);
+  if (kSplit) {
+    for (int k = 0; k < d; ++k)
+      for (int n = 0; n < f; ++n) {
+        const double w = a[static_cast<size_t>(k) * f + n];
+        const __nv_bfloat16 hi = __float2bfloat16_rn(static_cast<float>(w));
+        const __nv_bfloat16 lo = __float2bfloat16_rn(static_cast<float>(w - static_cast<double>(__bfloat162float(hi))));
+        T* row = we1.data() + static_cast<size_t>(n) * DK;
+        row[k] = cvt<T>(__bfloat162float(hi));
+        row[D + k] = cvt<T>(__bfloat162float(lo));
+        row[2 * D + k] = cvt<T>(__bfloat162float(hi));
+      }
+  } else {
+    pack_transposed(we1, 0, F, D, a, d, f, id_f, id_d);
+  }
   if (!need(f)) return fail(1, "weights too short (expert_b1)");
   for (int i = 0; i < f; ++i) be1[i] = static_cast<float>(a[i]);
   if (!need(static_cast<long long>(f) * tasks)) return fail(1, "weights too short (expert_w2)");
@@ -332,6 +349,7 @@ struct Pipe {
   Prof* prof = nullptr;
 
   Act* act(void* p) { return static_cast<Act*>(p); }
+  static constexpr int kSplitK = std::is_same<Act, __nv_bfloat16>::value ? 3 : 1;
 
   void mark(const char* name, double flops, double bytes) {
     if (!prof) return;
@@ -438,10 +456,11 @@ struct Pipe {
         cudaFuncSetAttribute(sumi_attention_tcgen05<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes);
         attr = true;
       }
+      dim3 tgrid((tiles + attn::kMaxTiles - 1) / attn::kMaxTiles, c->nh, c->G * e->R);
       if (hist)
-        sumi_attention_tcgen05<true><<<grid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
+        sumi_attention_tcgen05<true><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
       else
-        sumi_attention_tcgen05<false><<<grid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
+        sumi_attention_tcgen05<false><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
     } else {
       AttnArgsF32 a{};
       a.qkv = act(e->QKV); a.out = act(e->AO);
@@ -575,20 +594,21 @@ struct Pipe {
     // gated fusion over blocks (forward.py:143-156)
     {
       const long long n = Rc * (D / 4);
-      mark("gated_fusion", 0.0, static_cast<double>(Rc) * D * (4.0 * G + sizeof(Act)));
+      mark("gated_fusion", 0.0, static_cast<double>(Rc) * D * (4.0 * G + kSplitK * sizeof(Act)));
       gated_fusion_rows<Act><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-          Xcur + Rh * D, D, gD, G, c->gate_w, c->gate_b, act(e->Fz), D, static_cast<int>(Rc), D);
+          Xcur + Rh * D, D, gD, G, c->gate_w, c->gate_b, act(e->Fz), kSplitK * D, static_cast<int>(Rc), D);
       if (int rc = check()) return rc;
     }
     // expert heads (forward.py:159-166)
     gemm_name = "gemm_expert_w1";
-    if (int rc = gemm(act(e->Fz), D, 0, 1, act(c->we1), D, 0, static_cast<int>(Rc), F, D, 1, e->He, F, 0, 0, c->be1, 0,
-                      nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
+    // split-bf16 (bf16 mode): K = 3D over [Fz_hi|Fz_hi|Fz_lo] x [W_hi|W_lo|W_hi]; He kept fp32
+    if (int rc = gemm(act(e->Fz), kSplitK * D, 0, 1, act(c->we1), kSplitK * D, 0, static_cast<int>(Rc), F, kSplitK * D, 1,
+                      e->He, F, 0, 0, c->be1, 0, nullptr, 0, 0, EPI_BIAS | EPI_GELU | EPI_OUT_F32)) return rc;
     {
       const long long threads = Rc * 32;
-      mark("expert_out", 2.0 * Rc * F * c->tasks, static_cast<double>(Rc) * F * sizeof(Act));
-      expert_out_rows<Act><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
-          act(e->He), F, c->we2, c->be2, F, c->tasks, e->c_bkt, e->io.cand_len, e->io.out_offset,
+      mark("expert_out", 2.0 * Rc * F * c->tasks, static_cast<double>(Rc) * F * 4.0);
+      expert_out_rows<float><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+          static_cast<const float*>(e->He), F, c->we2, c->be2, F, c->tasks, e->c_bkt, e->io.cand_len, e->io.out_offset,
           e->io.scores, static_cast<int>(Rc));
       if (int rc = check()) return rc;
     }
@@ -752,8 +772,8 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
   e->Hf = A(G * rows * F * ab);
   e->Xa = static_cast<float*>(A(G * rows * D * 4));
   e->Xb = c->L > 1 ? static_cast<float*>(A(G * rows * D * 4)) : nullptr;
-  e->Fz = A(e->Rc * D * ab);
-  e->He = A(e->Rc * F * ab);
+  e->Fz = A(e->Rc * D * ab * (c->precision == FLAME_BF16 ? 3 : 1));
+  e->He = A(e->Rc * F * 4);
   e->spos = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
   e->ustart = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
   e->unique_ws = static_cast<long long*>(A(2 * static_cast<size_t>(R) * cap * 8));

@@ -3,6 +3,7 @@
 // sigmoid, and the history scatter into the block-major row space.
 #pragma once
 #include <cuda_bf16.h>
+#include <type_traits>
 #include "common.cuh"
 
 namespace flame {
@@ -99,7 +100,22 @@ __global__ void gated_fusion_rows(const float* __restrict__ xc, long long x_ld, 
     acc[2] = acc[2] + sigmoid_f(h.z * w.z + b.z) * h.z;
     acc[3] = acc[3] + sigmoid_f(h.w * w.w + b.w) * h.w;
   }
-  store4<TOut>(out + row * out_ld + c, acc[0], acc[1], acc[2], acc[3]);
+  if constexpr (std::is_same<TOut, __nv_bfloat16>::value) {
+    // split-bf16 operand for the expert GEMM: [hi | hi | lo] (row stride 3D),
+    // paired with weights [W_hi | W_lo | W_hi] -> hi*hi + hi*lo + lo*hi
+    float hi[4], lo[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      hi[q] = __bfloat162float(__float2bfloat16_rn(acc[q]));
+      lo[q] = acc[q] - hi[q];
+    }
+    TOut* o = out + row * out_ld + c;
+    store4<TOut>(o, hi[0], hi[1], hi[2], hi[3]);
+    store4<TOut>(o + D, hi[0], hi[1], hi[2], hi[3]);
+    store4<TOut>(o + 2 * D, lo[0], lo[1], lo[2], lo[3]);
+  } else {
+    store4<TOut>(out + row * out_ld + c, acc[0], acc[1], acc[2], acc[3]);
+  }
 }
 
 // Expert output, reference forward.py:165-166: sigmoid(hidden @ w2 + b2).

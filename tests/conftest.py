@@ -42,7 +42,8 @@ def golden_forward(name: str):
     return cfg, params, hist, cand, blob
 
 
-FORWARD_CASES = ["cfg1", "ref_instance", "sample_json", "l2_wide", "nohist", "l3_nb4", "cfg2", "cfg3"]
+FORWARD_CASES = ["cfg1", "ref_instance", "sample_json", "l2_wide", "nohist", "l3_nb4", "cfg2", "cfg3",
+                 "long_hist_l2", "cfg5"]
 SMALL_CASES = ["cfg1", "ref_instance", "sample_json", "l2_wide", "nohist", "l3_nb4"]
 
 
