@@ -1,27 +1,29 @@
 // SUMI attention on tcgen05 (reference model/attention.py:118-146 for the
 // candidate rows, :168-173 for the causal history rows of non-final layers).
 //
-// One CTA = (Climber block g, request r, head h) and up to kMaxTiles 128-row
-// query tiles of that request.  All candidates of a request read the SAME
-// history K/V of that request-block: it is loaded into shared memory once per
-// CTA (hb <= 256: resident for every tile; longer histories stream through a
-// two-slot ring) and never replicated per candidate.
+// Persistent kernel: each CTA walks units u = (request r, block g, head h) and
+// their 128-row query tiles ("jobs").  Jobs alternate between two softmax
+// warpgroups; each warpgroup has its OWN control thread that issues its TMA
+// loads and tcgen05 MMAs in a linear schedule, so the two pipelines run
+// independently: while one warpgroup computes a softmax, the tensor core works
+// on the other's QK^T / PV.
 //
-// The candidate's own key/value (the diagonal of the SUMI mask) seeds the
-// online-softmax state  m = s_self, l = 1, o = v_self;  every 128-key history
-// chunk then updates (m, l, o) as in the streaming softmax of attention_tiled
-// (attention.py:72-115).  H = 0 leaves the loop empty: out = v_self
-// (attention.py:131-133).
+// All candidates of a request read the SAME history K/V of that request-block
+// (never replicated per candidate): with hb <= 256 the whole K/V of the unit
+// stays resident in the warpgroup's two smem slots for all of its tiles of
+// that unit; longer histories stream 128-key chunks through the two slots.
+// The candidate's own key/value (the diagonal of the SUMI mask) arrives as TMA
+// tiles and seeds the online-softmax state  m = s_self, l = 1, o = v_self;
+// every history chunk then updates (m, l, o) like attention_tiled
+// (attention.py:72-115).  H = 0: no chunks, out = v_self (attention.py:131-133).
 //
-// Roles (288 threads):
-//   warps 0-3  softmax warpgroup 0 (TMEM lanes 0..127 = its query rows)
-//   warps 4-7  softmax warpgroup 1 (same lanes, second TMEM column range)
-//   warp 8     control: TMEM allocation, TMA loads, tcgen05.mma issue
-// The two warpgroups take alternating query tiles, so the MMAs of one overlap
-// the softmax of the other.  Per chunk and warpgroup:
-//   S = Q K^T (M=128 N=128 K=64) -> TMEM;  softmax rows (tcgen05.ld) -> P bf16
-//   in SW128 K-major smem;  O_j = P V (M=128 N=64 K=128, V consumed MN-major)
-//   -> TMEM;  o = o * alpha + O_j in registers.
+// Per chunk and warpgroup (TMEM columns of WG i: S [i*256, +128), P [+128, +64),
+// O [+192, +64)):
+//   S = Q K^T      tcgen05.mma SS, M=128 N=128 K=64          -> TMEM S
+//   softmax        1 thread = 1 query row (tcgen05.ld), exp2 -> bf16 P
+//   P -> TMEM      tcgen05.st (P never touches shared memory)
+//   O_j = P V      tcgen05.mma TS (A = P from TMEM, B = V MN-major smem), N=64
+//   o = o*alpha + O_j in registers.
 #pragma once
 #include "ptx.cuh"
 #include "common.cuh"
@@ -34,6 +36,7 @@ struct AttnArgs {
   long long qkv_gstride;     // elements per group
   long long out_ld, out_gstride;
   int DA;                    // attention width (heads * 64)
+  int nh;                    // heads
   int R;                     // requests in the batch
   int hb_bkt;                // history rows per (request, block) in the row space
   int c_bkt;                 // candidate rows per request in the row space
@@ -47,12 +50,12 @@ namespace attn {
 constexpr int kRows = 128;
 constexpr int kKeys = 128;
 constexpr int DH = 64;
-constexpr int kMaxTiles = 4;  // query tiles per CTA
-constexpr int kThreads = 288;
-constexpr int kTileBytes = kRows * DH * 2;  // 16 KB: Q tile, K chunk, V chunk
-constexpr int kPBytes = kRows * kKeys * 2;  // 32 KB: two SW128 sub-tiles
-constexpr int kSmemBytes = 2 * kTileBytes + 4 * kTileBytes + 2 * kPBytes + 1024 + 512;
-constexpr uint32_t kTmemCols = 512;  // per WG i: S at i*256 + [0,128), O at i*256 + [128,192)
+constexpr int kThreads = 320;  // WG0: warps 0-3, WG1: warps 4-7, control: warp 8 (WG0), warp 9 (WG1)
+constexpr int kTile = kRows * DH * 2;  // 16 KB
+// per warpgroup: Q, K_self, V_self, K[2], V[2]
+constexpr int kWGBytes = 7 * kTile;
+constexpr int kSmemBytes = 2 * kWGBytes + 1024 + 512;
+constexpr uint32_t kTmemCols = 512;
 }  // namespace attn
 
 template <bool kHist>
@@ -62,43 +65,26 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
-  uint8_t* sQ = smem;                       // [2] per warpgroup
-  uint8_t* sK = smem + 2 * kTileBytes;      // [2] slots
-  uint8_t* sV = smem + 4 * kTileBytes;      // [2] slots
-  uint8_t* sP = smem + 6 * kTileBytes;      // [2] per warpgroup
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * kTileBytes + 2 * kPBytes);
-  uint64_t* q_full = bars + 0;    // [2] per WG (TMA)
-  uint64_t* q_empty = bars + 2;   // [2] per WG (MMA commit)
-  uint64_t* k_full = bars + 4;    // [2] per slot (TMA)
-  uint64_t* v_full = bars + 6;    // [2] per slot (TMA)
-  uint64_t* kv_empty = bars + 8;  // [2] per slot (MMA commit)
-  uint64_t* s_full = bars + 10;   // [2] per WG (MMA commit)
-  uint64_t* o_full = bars + 12;   // [2] per WG (MMA commit)
-  uint64_t* p_full = bars + 14;   // [2] per WG (128 softmax threads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-
-  const int h = blockIdx.y;
-  const int g = blockIdx.z % a.num_blocks;
-  const int r = blockIdx.z / a.num_blocks;
-  const int hb = a.hist_len[r] / a.num_blocks;  // actual history rows of this request-block
-  const int hist_row0 = r * a.hb_bkt;
-  const int bkt = kHist ? a.hb_bkt : a.c_bkt;
-  const int n_tiles_total = (bkt + kRows - 1) / kRows;
-  const int tile0 = blockIdx.x * kMaxTiles;
-  const int n_tiles = min(kMaxTiles, n_tiles_total - tile0);
-  const int q_valid = kHist ? hb : a.cand_len[r];  // rows with local index < q_valid are real
-  const int q_base = kHist ? hist_row0 : a.R * a.hb_bkt + r * a.c_bkt;
-  const int nk_all = (hb + kKeys - 1) / kKeys;
-  const bool resident = nk_all <= 2;
-  auto chunks_of = [&](int tile) { return kHist ? min(nk_all, tile + 1) : nk_all; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kWGBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
 
   const int warp = threadIdx.x / 32;
-  const int qx = h * DH, kx = a.DA + h * DH, vx = 2 * a.DA + h * DH;
+  const int G = a.num_blocks;
+  const int n_units = a.R * G * a.nh;
+  const int bkt = kHist ? a.hb_bkt : a.c_bkt;
+  const int n_tiles = (bkt + kRows - 1) / kRows;
 
+  // barriers of warpgroup i: 11 each
+  auto B = [&](int i, int k) { return bars + i * 12 + k; };
+  // 0 q_full (tx)  1 qs_free (128 WG + 1 control)  2,3 k_full  4,5 v_full
+  // 6,7 kv_free (commit)  8 s_full (commit)  9 p_full (128)  10 o_full (commit)
   if (threadIdx.x == 256) {
     ptx::tma_prefetch_desc(&tm_qkv);
-    for (int i = 0; i < 14; ++i) ptx::mbar_init(&bars[i], 1);
-    for (int i = 14; i < 16; ++i) ptx::mbar_init(&bars[i], 128);
+    for (int i = 0; i < 2; ++i) {
+      for (int k = 0; k < 11; ++k) ptx::mbar_init(B(i, k), 1);
+      ptx::mbar_init(B(i, 1), 129);
+      ptx::mbar_init(B(i, 9), 128);
+    }
     ptx::fence_barrier_init();
   }
   if (warp == 8) ptx::tmem_alloc<kTmemCols>(tmem_slot);
@@ -107,123 +93,163 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (threadIdx.x == 256) {
-    // ------------------------------------------------------- control thread
+  // job q (per CTA) -> unit u = blockIdx.x + (q / n_tiles) * gridDim.x, tile t = q % n_tiles;
+  // warpgroup i takes jobs q = i, i + 2, ...
+  struct Job {
+    bool valid;
+    int u, r, g, h, t, hb, nk_all, nk, q_valid;
+    int hist_row0, q_row0;
+  };
+  auto job_at = [&](int q) {
+    Job j{};
+    j.u = blockIdx.x + (q / n_tiles) * gridDim.x;
+    j.valid = j.u < n_units;
+    if (!j.valid) return j;
+    j.t = q % n_tiles;
+    j.h = j.u % a.nh;
+    j.g = (j.u / a.nh) % G;
+    j.r = j.u / (a.nh * G);
+    j.hb = a.hist_len[j.r] / G;
+    j.nk_all = (j.hb + kKeys - 1) / kKeys;
+    j.nk = kHist ? min(j.nk_all, j.t + 1) : j.nk_all;
+    j.q_valid = kHist ? j.hb : a.cand_len[j.r];
+    j.hist_row0 = j.r * a.hb_bkt;
+    j.q_row0 = (kHist ? j.hist_row0 : a.R * a.hb_bkt + j.r * a.c_bkt) + j.t * kRows;
+    return j;
+  };
+
+  if (warp >= 8 && (threadIdx.x & 31) == 0) {
+    // --------------------------------------------- control thread of WG i
+    const int i = warp - 8;
+    uint8_t* base = smem + i * kWGBytes;
+    uint8_t *sQ = base, *sKs = base + kTile, *sVs = base + 2 * kTile;
+    uint8_t *sK = base + 3 * kTile, *sV = base + 5 * kTile;
+    const uint32_t tS = tmem + i * 256, tP = tS + 128, tO = tS + 192;
     constexpr uint32_t idesc_s = ptx::make_idesc_bf16(kRows, kKeys, 0, 0);
     constexpr uint32_t idesc_o = ptx::make_idesc_bf16(kRows, DH, 0, 1);
-    uint32_t kv_loads[2] = {0, 0};  // loads issued into each K/V slot
-    uint32_t kv_frees[2] = {0, 0};  // kv_empty completions consumed per slot
-    auto load_kv = [&](int j, int slot) {
-      ptx::mbar_arrive_expect_tx(&k_full[slot], kTileBytes);
-      ptx::tma_load_3d(sK + slot * kTileBytes, &tm_qkv, &k_full[slot], kx, hist_row0 + j * kKeys, g);
-      ptx::mbar_arrive_expect_tx(&v_full[slot], kTileBytes);
-      ptx::tma_load_3d(sV + slot * kTileBytes, &tm_qkv, &v_full[slot], vx, hist_row0 + j * kKeys, g);
+    uint32_t kv_loads[2] = {0, 0}, kv_frees[2] = {0, 0};
+    int res_unit = -1;  // unit whose K/V is resident in the slots (hb <= 256)
+    auto load_qs = [&](const Job& j) {
+      ptx::mbar_arrive_expect_tx(B(i, 0), (kHist ? 1 : 3) * kTile);
+      const int h = j.h;
+      ptx::tma_load_3d(sQ, &tm_qkv, B(i, 0), h * DH, j.q_row0, j.g);
+      if (!kHist) {
+        ptx::tma_load_3d(sKs, &tm_qkv, B(i, 0), a.DA + h * DH, j.q_row0, j.g);
+        ptx::tma_load_3d(sVs, &tm_qkv, B(i, 0), 2 * a.DA + h * DH, j.q_row0, j.g);
+      }
+    };
+    auto load_kv = [&](const Job& j, int chunk, int slot) {
+      if (kv_loads[slot] > kv_frees[slot]) {  // slot still read by earlier MMAs
+        ptx::mbar_wait(B(i, 6 + slot), kv_frees[slot] & 1);
+        ++kv_frees[slot];
+      }
+      const int row = j.hist_row0 + chunk * kKeys;
+      ptx::mbar_arrive_expect_tx(B(i, 2 + slot), kTile);
+      ptx::tma_load_3d(sK + slot * kTile, &tm_qkv, B(i, 2 + slot), a.DA + j.h * DH, row, j.g);
+      ptx::mbar_arrive_expect_tx(B(i, 4 + slot), kTile);
+      ptx::tma_load_3d(sV + slot * kTile, &tm_qkv, B(i, 4 + slot), 2 * a.DA + j.h * DH, row, j.g);
       ++kv_loads[slot];
     };
-    auto load_q = [&](int i, int tile) {
-      ptx::mbar_arrive_expect_tx(&q_full[i], kTileBytes);
-      ptx::tma_load_3d(sQ + i * kTileBytes, &tm_qkv, &q_full[i], qx, q_base + tile * kRows, g);
+    // K/V needed at the start of a job
+    auto prepare_kv = [&](const Job& j) {
+      if (j.nk_all <= 2) {
+        if (res_unit != j.u)
+          for (int c = 0; c < j.nk_all; ++c) load_kv(j, c, c);
+        res_unit = j.u;
+      } else {
+        res_unit = -1;
+        for (int c = 0; c < 2 && c < j.nk; ++c) load_kv(j, c, c);
+      }
     };
-    const int rounds = nk_all > 0 ? (n_tiles + 1) / 2 : 0;  // H = 0: no MMA work at all
-    for (int i = 0; i < 2 && i < n_tiles && rounds > 0; ++i) load_q(i, tile0 + i);
-    if (resident)
-      for (int j = 0; j < nk_all; ++j) load_kv(j, j);
-    uint32_t chunk_cnt[2] = {0, 0};  // chunks processed per WG (barrier phases)
-    for (int k = 0; k < rounds; ++k) {
-      const bool has_b = 2 * k + 1 < n_tiles;
-      const int nk[2] = {chunks_of(tile0 + 2 * k), has_b ? chunks_of(tile0 + 2 * k + 1) : 0};
-      const int nkr = max(nk[0], nk[1]);
-      if (!resident) {
-        for (int j = 0; j < 2 && j < nkr; ++j) {
-          if (kv_loads[j] > kv_frees[j]) {  // slot still read by the previous round's MMAs
-            ptx::mbar_wait(&kv_empty[j], kv_frees[j] & 1);
-            ++kv_frees[j];
-          }
-          load_kv(j, j);
-        }
-      }
-      for (int j = 0; j < nkr; ++j) {
-        const int slot = j & 1;
-        if (j == 0) {
-          ptx::mbar_wait(&q_full[0], k & 1);
-          if (has_b) ptx::mbar_wait(&q_full[1], k & 1);
-        }
-        ptx::mbar_wait(&k_full[slot], (kv_loads[slot] - 1) & 1);
+    Job cur = job_at(i);
+    if (cur.valid) {
+      load_qs(cur);
+      prepare_kv(cur);
+    }
+    uint32_t n = 0, cc = 0;  // jobs / chunks processed by this warpgroup
+    for (int q = i; cur.valid; q += 2, ++n) {
+      const Job nxt = job_at(q + 2);
+      const bool resident = cur.nk_all <= 2;
+      ptx::mbar_wait(B(i, 0), n & 1);  // Q (+ self tiles) landed
+      for (int c = 0; c < cur.nk; ++c, ++cc) {
+        const int slot = resident ? c : (c & 1);
+        ptx::mbar_wait(B(i, 2 + slot), (kv_loads[slot] - 1) & 1);
         ptx::tc_fence_after();
-        const uint32_t aK = ptx::smem_u32(sK + slot * kTileBytes);
-        for (int i = 0; i < 2; ++i) {
-          if (j >= nk[i]) continue;
-          const uint32_t aQ = ptx::smem_u32(sQ + i * kTileBytes);
+        const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK + slot * kTile);
 #pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk)
-            ptx::mma_bf16_ss(tmem + i * 256, ptx::make_desc_sw128(aQ + kk * 32, 16, 1024),
-                             ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
-          ptx::mma_commit(&s_full[i]);
-          if (j == nk[i] - 1) ptx::mma_commit(&q_empty[i]);  // Q_i no longer read this round
-        }
-        // prefetch the next round's Q as soon as this round's last S MMAs are done
-        for (int i = 0; i < 2; ++i) {
-          const int next = 2 * (k + 1) + i;
-          if (j == nk[i] - 1 && next < n_tiles) {
-            ptx::mbar_wait(&q_empty[i], k & 1);
-            load_q(i, tile0 + next);
+        for (int kk = 0; kk < DH / 16; ++kk)
+          ptx::mma_bf16_ss(tS, ptx::make_desc_sw128(aQ + kk * 32, 16, 1024),
+                           ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
+        ptx::mma_commit(B(i, 8));
+        if (c == cur.nk - 1) {
+          // last S of this job: once it completes (and the WG has read its
+          // q / self rows) the Q and self tiles can take the next job
+          ptx::mma_commit(B(i, 1));
+          if (nxt.valid) {
+            ptx::mbar_wait(B(i, 1), n & 1);
+            load_qs(nxt);
           }
         }
-        ptx::mbar_wait(&v_full[slot], (kv_loads[slot] - 1) & 1);
-        const uint32_t aV = ptx::smem_u32(sV + slot * kTileBytes);
-        for (int i = 0; i < 2; ++i) {
-          if (j >= nk[i]) continue;
-          ptx::mbar_wait(&p_full[i], chunk_cnt[i] & 1);  // S_i consumed, P_i written, O_i read
-          ptx::tc_fence_after();
-          const uint32_t aP = ptx::smem_u32(sP + i * kPBytes);
+        ptx::mbar_wait(B(i, 9), cc & 1);  // WG consumed S, stored P, read previous O
+        ptx::mbar_wait(B(i, 4 + slot), (kv_loads[slot] - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t aV = ptx::smem_u32(sV + slot * kTile);
 #pragma unroll
-          for (int kk = 0; kk < kKeys / 16; ++kk) {
-            const uint64_t ad = ptx::make_desc_sw128(aP + (kk >> 2) * (kRows * 128) + (kk & 3) * 32, 16, 1024);
-            const uint64_t bd = ptx::make_desc_sw128(aV + kk * 16 * 128, kRows * 128, 1024);
-            ptx::mma_bf16_ss(tmem + i * 256 + kKeys, ad, bd, idesc_o, kk != 0);
-          }
-          ptx::mma_commit(&o_full[i]);
-          ++chunk_cnt[i];
-        }
+        for (int kk = 0; kk < kKeys / 16; ++kk)
+          ptx::mma_bf16_ts(tO, tP + kk * 8, ptx::make_desc_sw128(aV + kk * 16 * 128, kRows * 128, 1024),
+                           idesc_o, kk != 0);
+        ptx::mma_commit(B(i, 10));
         if (!resident) {
-          ptx::mma_commit(&kv_empty[slot]);
-          if (j + 2 < nkr) {
-            ptx::mbar_wait(&kv_empty[slot], kv_frees[slot] & 1);
-            ++kv_frees[slot];
-            load_kv(j + 2, slot);
+          ptx::mma_commit(B(i, 6 + slot));
+          if (c + 2 < cur.nk) load_kv(cur, c + 2, slot);
+        } else if (c == cur.nk - 1 && !(nxt.valid && nxt.u == cur.u)) {
+          // unit done: every resident chunk's TMA must have landed (a causal tile
+          // may not have used all of them) before its slot can be recycled
+          for (int s = 0; s < cur.nk_all; ++s) {
+            ptx::mbar_wait(B(i, 2 + s), (kv_loads[s] - 1) & 1);
+            ptx::mbar_wait(B(i, 4 + s), (kv_loads[s] - 1) & 1);
+            ptx::mma_commit(B(i, 6 + s));
           }
         }
       }
+      if (cur.nk == 0) {
+        ptx::mbar_arrive(B(i, 1));
+        if (nxt.valid) {
+          ptx::mbar_wait(B(i, 1), n & 1);
+          load_qs(nxt);
+        }
+        if (resident && !(nxt.valid && nxt.u == cur.u)) res_unit = -1;
+      }
+      if (nxt.valid) prepare_kv(nxt);
+      cur = nxt;
     }
   } else if (warp < 8) {
     // ------------------------------------------------- softmax / epilogue rows
-    const int wg = warp >> 2;
-    const int i = threadIdx.x & 127;  // query row within the tile == TMEM lane
+    const int i = warp >> 2;
+    const int row = threadIdx.x & 127;  // query row within the tile == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + wg * 256 + lane_base, tO = tS + kKeys;
-    uint8_t* myP = sP + wg * kPBytes;
-    const float sl2 = a.scale_log2[g];
-    uint32_t cnt = 0;
-    for (int t = wg; t < n_tiles; t += 2) {
-      const int tile = tile0 + t;
-      const int qi = tile * kRows + i;
-      const bool in_region = qi < bkt;  // rows past the request's region are never touched
-      const bool row_ok = qi < q_valid;
-      const long long grow = q_base + (in_region ? qi : 0);
-      const __nv_bfloat16* base = a.qkv + g * a.qkv_gstride + grow * (3LL * a.DA);
+    const uint32_t tS = tmem + i * 256 + lane_base, tP = tS + 128, tO = tS + 192;
+    const uint8_t* base = smem + i * kWGBytes;
+    const uint8_t *sQ = base, *sKs = base + kTile, *sVs = base + 2 * kTile;
+    uint32_t n = 0, cc = 0;
+    for (int q = i;; q += 2, ++n) {
+      const Job j = job_at(q);
+      if (!j.valid) break;
+      const int qi = j.t * kRows + row;
+      const bool row_ok = qi < j.q_valid;
+      const float sl2 = a.scale_log2[j.g];
       float o[DH];
       float m, l;
+      ptx::mbar_wait(B(i, 0), n & 1);
       if (!kHist) {
         // self term: s_self = q . k_self (attention.py:134) seeds the state
         float dot = 0.f;
 #pragma unroll
         for (int c = 0; c < DH / 8; ++c) {
-          uint4 qv = make_uint4(0, 0, 0, 0), kv = qv, vv = qv;
-          if (in_region) {
-            qv = *reinterpret_cast<const uint4*>(base + qx + c * 8);
-            kv = *reinterpret_cast<const uint4*>(base + kx + c * 8);
-            vv = *reinterpret_cast<const uint4*>(base + vx + c * 8);
-          }
+          const uint32_t off = ptx::sw128_offset(row, c * 16);
+          const uint4 qv = *reinterpret_cast<const uint4*>(sQ + off);
+          const uint4 kv = *reinterpret_cast<const uint4*>(sKs + off);
+          const uint4 vv = *reinterpret_cast<const uint4*>(sVs + off);
           const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qv);
           const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
           const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vv);
@@ -246,20 +272,19 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
 #pragma unroll
         for (int e = 0; e < DH; ++e) o[e] = 0.f;
       }
-      const int nk = chunks_of(tile);
-      for (int j = 0; j < nk; ++j, ++cnt) {
-        const int key0 = j * kKeys;
-        int key_lim = hb - key0;  // keys with local index < key_lim are valid
+      ptx::mbar_arrive(B(i, 1));  // q / self rows read
+      for (int c = 0; c < j.nk; ++c, ++cc) {
+        const int key0 = c * kKeys;
+        int key_lim = j.hb - key0;  // keys with local index < key_lim are valid
         if (kHist) key_lim = min(key_lim, qi - key0 + 1);
         const bool full = key_lim >= kKeys;
-        ptx::mbar_wait(&s_full[wg], cnt & 1);
+        ptx::mbar_wait(B(i, 8), cc & 1);
         ptx::tc_fence_after();
-        // pass 1: chunk max
         float cmax = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < kKeys / 32; ++c) {
+        for (int k = 0; k < kKeys / 32; ++k) {
           uint32_t s[32];
-          ptx::tmem_ld_32x32b_x32(tS + c * 32, s);
+          ptx::tmem_ld_32x32b_x32(tS + k * 32, s);
           ptx::tmem_ld_wait();
           if (full) {
 #pragma unroll
@@ -267,18 +292,17 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           } else {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
-              if (c * 32 + e < key_lim) cmax = fmaxf(cmax, __uint_as_float(s[e]));
+              if (k * 32 + e < key_lim) cmax = fmaxf(cmax, __uint_as_float(s[e]));
           }
         }
         const float m_new = fmaxf(m, cmax * sl2);
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
         const float alpha = (m == -INFINITY) ? 0.f : ptx::exp2_approx(m - m_use);
-        // pass 2: p = exp2(s*scale - m) -> bf16 P (SW128 K-major, 2 sub-tiles of 64 keys)
         float psum = 0.f;
 #pragma unroll
-        for (int c = 0; c < kKeys / 32; ++c) {
+        for (int k = 0; k < kKeys / 32; ++k) {
           uint32_t s[32];
-          ptx::tmem_ld_32x32b_x32(tS + c * 32, s);
+          ptx::tmem_ld_32x32b_x32(tS + k * 32, s);
           ptx::tmem_ld_wait();
           uint32_t packed[16];
 #pragma unroll
@@ -286,39 +310,34 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
             float p0 = ptx::exp2_approx(fmaf(__uint_as_float(s[e]), sl2, -m_use));
             float p1 = ptx::exp2_approx(fmaf(__uint_as_float(s[e + 1]), sl2, -m_use));
             if (!full) {
-              p0 = (c * 32 + e < key_lim) ? p0 : 0.f;
-              p1 = (c * 32 + e + 1 < key_lim) ? p1 : 0.f;
+              p0 = (k * 32 + e < key_lim) ? p0 : 0.f;
+              p1 = (k * 32 + e + 1 < key_lim) ? p1 : 0.f;
             }
             psum += p0 + p1;
             packed[e / 2] = pack_bf16x2(p0, p1);
           }
-          uint8_t* sub = myP + (c >> 1) * (kRows * 128);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<uint4*>(sub + ptx::sw128_offset(i, (c & 1) * 64 + q * 16)) =
-                make_uint4(packed[q * 4], packed[q * 4 + 1], packed[q * 4 + 2], packed[q * 4 + 3]);
+          ptx::tmem_st_32x32b_x16(tP + k * 16, packed);
         }
+        ptx::tmem_st_wait();
         ptx::tc_fence_before();
-        ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&p_full[wg]);
+        ptx::mbar_arrive(B(i, 9));
         l = l * alpha + psum;
         m = m_new;
-        // O_j = P V
-        ptx::mbar_wait(&o_full[wg], cnt & 1);
+        ptx::mbar_wait(B(i, 10), cc & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < DH / 32; ++c) {
+        for (int k = 0; k < DH / 32; ++k) {
           uint32_t ov[32];
-          ptx::tmem_ld_32x32b_x32(tO + c * 32, ov);
+          ptx::tmem_ld_32x32b_x32(tO + k * 32, ov);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[c * 32 + e] = fmaf(o[c * 32 + e], alpha, __uint_as_float(ov[e]));
+          for (int e = 0; e < 32; ++e) o[k * 32 + e] = fmaf(o[k * 32 + e], alpha, __uint_as_float(ov[e]));
         }
         ptx::tc_fence_before();
       }
       if (row_ok) {
         const float inv = 1.f / l;
-        __nv_bfloat16* dst = a.out + g * a.out_gstride + grow * a.out_ld + h * DH;
+        __nv_bfloat16* dst = a.out + j.g * a.out_gstride + static_cast<long long>(j.q_row0 + row) * a.out_ld + j.h * DH;
 #pragma unroll
         for (int c = 0; c < DH / 8; ++c) {
           uint4 w;

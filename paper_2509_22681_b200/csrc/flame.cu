@@ -456,7 +456,9 @@ struct Pipe {
         cudaFuncSetAttribute(sumi_attention_tcgen05<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes);
         attr = true;
       }
-      dim3 tgrid((tiles + attn::kMaxTiles - 1) / attn::kMaxTiles, c->nh, c->G * e->R);
+      a.nh = c->nh;
+      const int units = e->R * c->G * c->nh;  // persistent: one CTA per SM walks the units
+      dim3 tgrid(units < c->num_sms ? units : c->num_sms);
       if (hist)
         sumi_attention_tcgen05<true><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
       else
