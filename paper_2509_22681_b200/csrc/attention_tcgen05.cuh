@@ -12,18 +12,21 @@
 // (never replicated per candidate): with hb <= 256 the whole K/V of the unit
 // stays resident in the warpgroup's two smem slots for all of its tiles of
 // that unit; longer histories stream 128-key chunks through the two slots.
-// The candidate's own key/value (the diagonal of the SUMI mask) arrives as TMA
-// tiles and seeds the online-softmax state  m = s_self, l = 1, o = v_self;
-// every history chunk then updates (m, l, o) like attention_tiled
-// (attention.py:72-115).  H = 0: no chunks, out = v_self (attention.py:131-133).
 //
-// Per chunk and warpgroup (TMEM columns of WG i: S [i*256, +128), P [+128, +64),
-// O [+192, +64)):
-//   S = Q K^T      tcgen05.mma SS, M=128 N=128 K=64          -> TMEM S
-//   softmax        1 thread = 1 query row (tcgen05.ld), exp2 -> bf16 P
-//   P -> TMEM      tcgen05.st (P never touches shared memory)
-//   O_j = P V      tcgen05.mma TS (A = P from TMEM, B = V MN-major smem), N=64
-//   o = o*alpha + O_j in registers.
+// Softmax (1 thread = 1 query row).  The candidate's own key (the diagonal of
+// the SUMI mask) seeds the state: m = s_self, l = 1.  History chunks update a
+// reference max m that is only raised when a chunk max exceeds it by more than
+// 2^8 (then the TMEM accumulator O is rescaled by the warp); otherwise
+// p = exp2(s - m) stays within [0, 2^8] and O keeps accumulating in TMEM across
+// chunks (PV with accumulate = 1).  At the end
+//   out = (O + exp2(s_self - m) * v_self) / l,
+// which equals attention_sumi_candidates' softmax over [history | self]
+// (attention.py:131-146); H = 0 gives out = v_self.
+//
+// TMEM columns of warpgroup i: S [i*256, +128), P [+128, +64), O [+192, +64).
+//   S = Q K^T      tcgen05.mma SS, M=128 N=128 K=64
+//   P -> TMEM      tcgen05.st of the bf16 probabilities (never touches smem)
+//   O += P V       tcgen05.mma TS (A = P from TMEM, B = V MN-major smem), N=64
 #pragma once
 #include "ptx.cuh"
 #include "common.cuh"
@@ -46,6 +49,18 @@ struct AttnArgs {
   const float* scale_log2;   // [G] log2(e) / (tau_g * sqrt(head_dim))
 };
 
+// Debug-only event trace of CTA 0 (set through flame_debug_attn_trace): slot 0/1 =
+// warpgroup rows 0, slot 2/3 = their control threads; entry = clock64 << 8 | code.
+__device__ unsigned long long* g_attn_trace = nullptr;
+__device__ unsigned int g_attn_trace_n[4];
+#define ATTN_TRACE(slot, code)                                                            \
+  do {                                                                                    \
+    if (g_attn_trace != nullptr && blockIdx.x == 0 && ((slot) >= 2 ? (threadIdx.x & 31) == 0 : (threadIdx.x & 127) == 0)) { \
+      const unsigned int k_ = atomicAdd(&g_attn_trace_n[slot], 1u);                        \
+      if (k_ < 4096) g_attn_trace[(slot) * 4096 + k_] = (clock64() << 8) | (code);         \
+    }                                                                                     \
+  } while (0)
+
 namespace attn {
 constexpr int kRows = 128;
 constexpr int kKeys = 128;
@@ -56,6 +71,7 @@ constexpr int kTile = kRows * DH * 2;  // 16 KB
 constexpr int kWGBytes = 7 * kTile;
 constexpr int kSmemBytes = 2 * kWGBytes + 1024 + 512;
 constexpr uint32_t kTmemCols = 512;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
 }  // namespace attn
 
 template <bool kHist>
@@ -74,10 +90,10 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
   const int bkt = kHist ? a.hb_bkt : a.c_bkt;
   const int n_tiles = (bkt + kRows - 1) / kRows;
 
-  // barriers of warpgroup i: 11 each
-  auto B = [&](int i, int k) { return bars + i * 12 + k; };
+  // barriers of warpgroup i (12 slots each):
   // 0 q_full (tx)  1 qs_free (128 WG + 1 control)  2,3 k_full  4,5 v_full
   // 6,7 kv_free (commit)  8 s_full (commit)  9 p_full (128)  10 o_full (commit)
+  auto B = [&](int i, int k) { return bars + i * 12 + k; };
   if (threadIdx.x == 256) {
     ptx::tma_prefetch_desc(&tm_qkv);
     for (int i = 0; i < 2; ++i) {
@@ -109,18 +125,21 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     j.h = j.u % a.nh;
     j.g = (j.u / a.nh) % G;
     j.r = j.u / (a.nh * G);
-    j.hb = a.hist_len[j.r] / G;
+    j.hb = __ldg(a.hist_len + j.r) / G;
     j.nk_all = (j.hb + kKeys - 1) / kKeys;
     j.nk = kHist ? min(j.nk_all, j.t + 1) : j.nk_all;
-    j.q_valid = kHist ? j.hb : a.cand_len[j.r];
+    j.q_valid = kHist ? j.hb : __ldg(a.cand_len + j.r);
     j.hist_row0 = j.r * a.hb_bkt;
     j.q_row0 = (kHist ? j.hist_row0 : a.R * a.hb_bkt + j.r * a.c_bkt) + j.t * kRows;
     return j;
   };
 
-  if (warp >= 8 && (threadIdx.x & 31) == 0) {
-    // --------------------------------------------- control thread of WG i
+  if (warp >= 8) {
+    // ---------------------------------------------- control warp of WG i
+    // The whole warp runs the schedule (waits, bookkeeping) so every operand
+    // stays warp-uniform; one elected lane issues TMA / MMA / commits.
     const int i = warp - 8;
+    const bool leader = ptx::elect_one();
     uint8_t* base = smem + i * kWGBytes;
     uint8_t *sQ = base, *sKs = base + kTile, *sVs = base + 2 * kTile;
     uint8_t *sK = base + 3 * kTile, *sV = base + 5 * kTile;
@@ -130,13 +149,16 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     uint32_t kv_loads[2] = {0, 0}, kv_frees[2] = {0, 0};
     int res_unit = -1;  // unit whose K/V is resident in the slots (hb <= 256)
     auto load_qs = [&](const Job& j) {
-      ptx::mbar_arrive_expect_tx(B(i, 0), (kHist ? 1 : 3) * kTile);
-      const int h = j.h;
-      ptx::tma_load_3d(sQ, &tm_qkv, B(i, 0), h * DH, j.q_row0, j.g);
-      if (!kHist) {
-        ptx::tma_load_3d(sKs, &tm_qkv, B(i, 0), a.DA + h * DH, j.q_row0, j.g);
-        ptx::tma_load_3d(sVs, &tm_qkv, B(i, 0), 2 * a.DA + h * DH, j.q_row0, j.g);
+      if (leader) {
+        ptx::mbar_arrive_expect_tx(B(i, 0), (kHist ? 1 : 3) * kTile);
+        const int h = j.h;
+        ptx::tma_load_3d(sQ, &tm_qkv, B(i, 0), h * DH, j.q_row0, j.g);
+        if (!kHist) {
+          ptx::tma_load_3d(sKs, &tm_qkv, B(i, 0), a.DA + h * DH, j.q_row0, j.g);
+          ptx::tma_load_3d(sVs, &tm_qkv, B(i, 0), 2 * a.DA + h * DH, j.q_row0, j.g);
+        }
       }
+      __syncwarp();
     };
     auto load_kv = [&](const Job& j, int chunk, int slot) {
       if (kv_loads[slot] > kv_frees[slot]) {  // slot still read by earlier MMAs
@@ -144,10 +166,13 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
         ++kv_frees[slot];
       }
       const int row = j.hist_row0 + chunk * kKeys;
-      ptx::mbar_arrive_expect_tx(B(i, 2 + slot), kTile);
-      ptx::tma_load_3d(sK + slot * kTile, &tm_qkv, B(i, 2 + slot), a.DA + j.h * DH, row, j.g);
-      ptx::mbar_arrive_expect_tx(B(i, 4 + slot), kTile);
-      ptx::tma_load_3d(sV + slot * kTile, &tm_qkv, B(i, 4 + slot), 2 * a.DA + j.h * DH, row, j.g);
+      if (leader) {
+        ptx::mbar_arrive_expect_tx(B(i, 2 + slot), kTile);
+        ptx::tma_load_3d(sK + slot * kTile, &tm_qkv, B(i, 2 + slot), a.DA + j.h * DH, row, j.g);
+        ptx::mbar_arrive_expect_tx(B(i, 4 + slot), kTile);
+        ptx::tma_load_3d(sV + slot * kTile, &tm_qkv, B(i, 4 + slot), 2 * a.DA + j.h * DH, row, j.g);
+      }
+      __syncwarp();
       ++kv_loads[slot];
     };
     // K/V needed at the start of a job
@@ -169,38 +194,49 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     uint32_t n = 0, cc = 0;  // jobs / chunks processed by this warpgroup
     for (int q = i; cur.valid; q += 2, ++n) {
       const Job nxt = job_at(q + 2);
+      ATTN_TRACE(2 + i, 11);
       const bool resident = cur.nk_all <= 2;
       ptx::mbar_wait(B(i, 0), n & 1);  // Q (+ self tiles) landed
-      for (int c = 0; c < cur.nk; ++c, ++cc) {
+      ATTN_TRACE(2 + i, 12);
+      const uint32_t aQ = ptx::smem_u32(sQ);
+      auto issue_s = [&](int c) {  // S = Q K_c^T into the WG's S columns
         const int slot = resident ? c : (c & 1);
         ptx::mbar_wait(B(i, 2 + slot), (kv_loads[slot] - 1) & 1);
         ptx::tc_fence_after();
-        const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK + slot * kTile);
+        const uint32_t aK = ptx::smem_u32(sK + slot * kTile);
+        if (leader) {
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          ptx::mma_bf16_ss(tS, ptx::make_desc_sw128(aQ + kk * 32, 16, 1024),
-                           ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
-        ptx::mma_commit(B(i, 8));
-        if (c == cur.nk - 1) {
-          // last S of this job: once it completes (and the WG has read its
-          // q / self rows) the Q and self tiles can take the next job
-          ptx::mma_commit(B(i, 1));
-          if (nxt.valid) {
-            ptx::mbar_wait(B(i, 1), n & 1);
-            load_qs(nxt);
-          }
+          for (int kk = 0; kk < DH / 16; ++kk)
+            ptx::mma_bf16_ss(tS, ptx::make_desc_sw128(aQ + kk * 32, 16, 1024),
+                             ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
+          ptx::mma_commit(B(i, 8));
+          if (c == cur.nk - 1) ptx::mma_commit(B(i, 1));  // last read of Q this job
         }
-        ptx::mbar_wait(B(i, 9), cc & 1);  // WG consumed S, stored P, read previous O
+        __syncwarp();
+        ATTN_TRACE(2 + i, 13);
+      };
+      if (cur.nk > 0) issue_s(0);
+      for (int c = 0; c < cur.nk; ++c, ++cc) {
+        const int slot = resident ? c : (c & 1);
+        ptx::mbar_wait(B(i, 9), cc & 1);  // WG consumed S_c, stored P_c (and rescaled O)
+        ATTN_TRACE(2 + i, 14);
+        // S_{c+1} first: the warpgroup needs it next; PV_c is only needed at job end
+        if (c + 1 < cur.nk) issue_s(c + 1);
         ptx::mbar_wait(B(i, 4 + slot), (kv_loads[slot] - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t aV = ptx::smem_u32(sV + slot * kTile);
+        if (leader) {
 #pragma unroll
-        for (int kk = 0; kk < kKeys / 16; ++kk)
-          ptx::mma_bf16_ts(tO, tP + kk * 8, ptx::make_desc_sw128(aV + kk * 16 * 128, kRows * 128, 1024),
-                           idesc_o, kk != 0);
-        ptx::mma_commit(B(i, 10));
+          for (int kk = 0; kk < kKeys / 16; ++kk)
+            ptx::mma_bf16_ts(tO, tP + kk * 8, ptx::make_desc_sw128(aV + kk * 16 * 128, kRows * 128, 1024),
+                             idesc_o, 1u);  // O was seeded by the warpgroup
+          ptx::mma_commit(B(i, 10));
+        }
+        __syncwarp();
+        ATTN_TRACE(2 + i, 15);
         if (!resident) {
-          ptx::mma_commit(B(i, 6 + slot));
+          if (leader) ptx::mma_commit(B(i, 6 + slot));
+          __syncwarp();
           if (c + 2 < cur.nk) load_kv(cur, c + 2, slot);
         } else if (c == cur.nk - 1 && !(nxt.valid && nxt.u == cur.u)) {
           // unit done: every resident chunk's TMA must have landed (a causal tile
@@ -208,17 +244,23 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           for (int s = 0; s < cur.nk_all; ++s) {
             ptx::mbar_wait(B(i, 2 + s), (kv_loads[s] - 1) & 1);
             ptx::mbar_wait(B(i, 4 + s), (kv_loads[s] - 1) & 1);
-            ptx::mma_commit(B(i, 6 + s));
+            if (leader) ptx::mma_commit(B(i, 6 + s));
+            __syncwarp();
           }
         }
       }
+      // Q / self tiles are free once the last S completed and the WG read its rows
+      if (cur.nk > 0 && nxt.valid) {
+        ptx::mbar_wait(B(i, 1), n & 1);
+        load_qs(nxt);
+      }
       if (cur.nk == 0) {
-        ptx::mbar_arrive(B(i, 1));
+        if (leader) ptx::mbar_arrive(B(i, 1));
+        __syncwarp();
         if (nxt.valid) {
           ptx::mbar_wait(B(i, 1), n & 1);
           load_qs(nxt);
         }
-        if (resident && !(nxt.valid && nxt.u == cur.u)) res_unit = -1;
       }
       if (nxt.valid) prepare_kv(nxt);
       cur = nxt;
@@ -232,17 +274,22 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     const uint8_t* base = smem + i * kWGBytes;
     const uint8_t *sQ = base, *sKs = base + kTile, *sVs = base + 2 * kTile;
     uint32_t n = 0, cc = 0;
+    Job nj = job_at(i);
     for (int q = i;; q += 2, ++n) {
-      const Job j = job_at(q);
+      const Job j = nj;
+      ATTN_TRACE(i, 1);
       if (!j.valid) break;
+      nj = job_at(q + 2);  // metadata loads overlap this job
       const int qi = j.t * kRows + row;
       const bool row_ok = qi < j.q_valid;
       const float sl2 = a.scale_log2[j.g];
-      float o[DH];
-      float m, l;
+      float m_self, m, l;
+      uint32_t seed[DH];
       ptx::mbar_wait(B(i, 0), n & 1);
+      ATTN_TRACE(i, 2);
+      // seed the TMEM accumulator O with v_self (weight exp2(s_self - m) = 1 at
+      // m = s_self); history rows start from O = 0, m = -inf, l = 0
       if (!kHist) {
-        // self term: s_self = q . k_self (attention.py:134) seeds the state
         float dot = 0.f;
 #pragma unroll
         for (int c = 0; c < DH / 8; ++c) {
@@ -257,84 +304,110 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           for (int e = 0; e < 4; ++e) {
             const float2 qf = __bfloat1622float2(q2[e]);
             const float2 kf = __bfloat1622float2(k2[e]);
-            const float2 vf = __bfloat1622float2(v2[e]);
             dot = fmaf(qf.x, kf.x, dot);
             dot = fmaf(qf.y, kf.y, dot);
-            o[c * 8 + e * 2] = vf.x;
-            o[c * 8 + e * 2 + 1] = vf.y;
+            const float2 v = __bfloat1622float2(v2[e]);
+            seed[c * 8 + 2 * e] = __float_as_uint(v.x);
+            seed[c * 8 + 2 * e + 1] = __float_as_uint(v.y);
           }
         }
-        m = dot * sl2;
+        m_self = dot * sl2;
+        m = m_self;
         l = 1.f;
       } else {
+#pragma unroll
+        for (int e = 0; e < DH; ++e) seed[e] = 0u;
+        m_self = -INFINITY;
         m = -INFINITY;
         l = 0.f;
-#pragma unroll
-        for (int e = 0; e < DH; ++e) o[e] = 0.f;
       }
+#pragma unroll
+      for (int k = 0; k < DH / 16; ++k)
+        ptx::tmem_st_32x32b_x16(tO + k * 16, *reinterpret_cast<uint32_t(*)[16]>(seed + k * 16));
       ptx::mbar_arrive(B(i, 1));  // q / self rows read
       for (int c = 0; c < j.nk; ++c, ++cc) {
         const int key0 = c * kKeys;
         int key_lim = j.hb - key0;  // keys with local index < key_lim are valid
         if (kHist) key_lim = min(key_lim, qi - key0 + 1);
-        const bool full = key_lim >= kKeys;
+        const bool full = __all_sync(0xffffffffu, key_lim >= kKeys);
         ptx::mbar_wait(B(i, 8), cc & 1);
+        ATTN_TRACE(i, 3);
         ptx::tc_fence_after();
+        // the whole 128-key row of S in registers: 4 loads, one wait
+        uint32_t s[kKeys];
+#pragma unroll
+        for (int k = 0; k < kKeys / 32; ++k)
+          ptx::tmem_ld_32x32b_x32(tS + k * 32, *reinterpret_cast<uint32_t(*)[32]>(s + k * 32));
+        ptx::tmem_ld_wait();
+        if (!full) {
+#pragma unroll
+          for (int e = 0; e < kKeys; ++e)
+            if (e >= key_lim) s[e] = __float_as_uint(-INFINITY);
+        }
         float cmax = -INFINITY;
 #pragma unroll
-        for (int k = 0; k < kKeys / 32; ++k) {
-          uint32_t s[32];
-          ptx::tmem_ld_32x32b_x32(tS + k * 32, s);
-          ptx::tmem_ld_wait();
-          if (full) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) cmax = fmaxf(cmax, __uint_as_float(s[e]));
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (k * 32 + e < key_lim) cmax = fmaxf(cmax, __uint_as_float(s[e]));
-          }
-        }
-        const float m_new = fmaxf(m, cmax * sl2);
-        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        const float alpha = (m == -INFINITY) ? 0.f : ptx::exp2_approx(m - m_use);
+        for (int e = 0; e < kKeys; ++e) cmax = fmaxf(cmax, __uint_as_float(s[e]));
+        // raise the reference max only when the chunk max exceeds it by > 2^8
+        const float cm = cmax * sl2;
+        const bool raise = (m == -INFINITY) ? (cm != -INFINITY) : (cm - m > kRescaleThreshold);
+        const float m_new = raise ? cm : m;
+        const float alpha = (raise && m != -INFINITY) ? ptx::exp2_approx(m - m_new) : 1.f;
+        m = m_new;
+        const float m_use = (m == -INFINITY) ? 0.f : m;
+        // p = exp2(s*scale - m), packed to bf16 pairs in place (s[e/2] is dead)
         float psum = 0.f;
 #pragma unroll
-        for (int k = 0; k < kKeys / 32; ++k) {
-          uint32_t s[32];
-          ptx::tmem_ld_32x32b_x32(tS + k * 32, s);
-          ptx::tmem_ld_wait();
-          uint32_t packed[16];
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float p0 = ptx::exp2_approx(fmaf(__uint_as_float(s[e]), sl2, -m_use));
-            float p1 = ptx::exp2_approx(fmaf(__uint_as_float(s[e + 1]), sl2, -m_use));
-            if (!full) {
-              p0 = (k * 32 + e < key_lim) ? p0 : 0.f;
-              p1 = (k * 32 + e + 1 < key_lim) ? p1 : 0.f;
-            }
-            psum += p0 + p1;
-            packed[e / 2] = pack_bf16x2(p0, p1);
-          }
-          ptx::tmem_st_32x32b_x16(tP + k * 16, packed);
+        for (int e = 0; e < kKeys; e += 2) {
+          const float p0 = ptx::exp2_approx(fmaf(__uint_as_float(s[e]), sl2, -m_use));
+          const float p1 = ptx::exp2_approx(fmaf(__uint_as_float(s[e + 1]), sl2, -m_use));
+          psum += p0 + p1;
+          s[e / 2] = pack_bf16x2(p0, p1);
         }
+        l = l * alpha + psum;
+        // PV(c-1) must be done before P is overwritten and O rescaled
+        if (c > 0) {
+          ptx::mbar_wait(B(i, 10), (cc - 1) & 1);
+          ptx::tc_fence_after();
+        }
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          uint32_t ov[DH];
+#pragma unroll
+          for (int k = 0; k < DH / 32; ++k)
+            ptx::tmem_ld_32x32b_x32(tO + k * 32, *reinterpret_cast<uint32_t(*)[32]>(ov + k * 32));
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < DH; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k)
+            ptx::tmem_st_32x32b_x16(tO + k * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + k * 16));
+        }
+#pragma unroll
+        for (int k = 0; k < kKeys / 32; ++k)
+          ptx::tmem_st_32x32b_x16(tP + k * 16, *reinterpret_cast<uint32_t(*)[16]>(s + k * 16));
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(B(i, 9));
-        l = l * alpha + psum;
-        m = m_new;
-        ptx::mbar_wait(B(i, 10), cc & 1);
+        ATTN_TRACE(i, 4);
+      }
+      // out = O / l  (O already holds exp2(s_self - m) v_self)
+      float o[DH];
+      if (j.nk > 0) {
+        ptx::mbar_wait(B(i, 10), (cc - 1) & 1);
         ptx::tc_fence_after();
+      } else {
+        ptx::tmem_st_wait();
+      }
+      {
+        uint32_t ov[DH];
 #pragma unroll
-        for (int k = 0; k < DH / 32; ++k) {
-          uint32_t ov[32];
-          ptx::tmem_ld_32x32b_x32(tO + k * 32, ov);
-          ptx::tmem_ld_wait();
+        for (int k = 0; k < DH / 32; ++k)
+          ptx::tmem_ld_32x32b_x32(tO + k * 32, *reinterpret_cast<uint32_t(*)[32]>(ov + k * 32));
+        ptx::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[k * 32 + e] = fmaf(o[k * 32 + e], alpha, __uint_as_float(ov[e]));
-        }
+        for (int e = 0; e < DH; ++e) o[e] = __uint_as_float(ov[e]);
         ptx::tc_fence_before();
       }
+      ATTN_TRACE(i, 5);
       if (row_ok) {
         const float inv = 1.f / l;
         __nv_bfloat16* dst = a.out + j.g * a.out_gstride + static_cast<long long>(j.q_row0 + row) * a.out_ld + j.h * DH;

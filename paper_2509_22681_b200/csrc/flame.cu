@@ -897,3 +897,13 @@ void* flame_exec_workspace(FlameExec* e, const char* name) {
 }
 
 }  // extern "C"
+
+// Debug-only (not part of the public header): route the attention kernel's CTA-0
+// event trace into a caller-owned device buffer of 4 x 4096 uint64 (NULL = off).
+extern "C" int flame_debug_attn_trace(void* dev_buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
+  CUDA_TRY(cudaMemcpyToSymbol(flame::g_attn_trace, &p, sizeof(p)));
+  unsigned int zeros[4] = {0, 0, 0, 0};
+  CUDA_TRY(cudaMemcpyToSymbol(flame::g_attn_trace_n, zeros, sizeof(zeros)));
+  return 0;
+}

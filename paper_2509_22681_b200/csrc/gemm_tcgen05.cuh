@@ -109,8 +109,10 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
 
   const int total_tiles = groups * m_tiles * n_tiles;
 
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     // ------------------------------------------------------------ producer
+    // whole warp walks the schedule (operands stay warp-uniform); one lane issues
+    const bool leader = ptx::elect_one();
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
@@ -120,16 +122,20 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
       const int ga = a_shared ? 0 : g;
       for (int kb = 0; kb < num_k_blocks; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-        ptx::tma_load_3d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * gemm::BK,
-                         m_blk * gemm::BM, ga);
-        ptx::tma_load_3d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * gemm::BK,
-                         n_blk * BN, g);
+        if (leader) {
+          ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          ptx::tma_load_3d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * gemm::BK,
+                           m_blk * gemm::BM, ga);
+          ptx::tma_load_3d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * gemm::BK,
+                           n_blk * BN, g);
+        }
+        __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (threadIdx.x == 32) {
+  } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer
+    const bool leader = ptx::elect_one();
     constexpr uint32_t idesc = ptx::make_idesc_bf16(gemm::BM, BN, 0, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -144,16 +150,20 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
         ptx::tc_fence_after();
         const uint32_t a_addr = ptx::smem_u32(smem_a + stage * C::kABytes);
         const uint32_t b_addr = ptx::smem_u32(smem_b + stage * C::kBBytes);
+        if (leader) {
 #pragma unroll
-        for (int k = 0; k < gemm::BK / 16; ++k) {
-          const uint64_t ad = ptx::make_desc_sw128(a_addr + k * 32, 16, 1024);
-          const uint64_t bd = ptx::make_desc_sw128(b_addr + k * 32, 16, 1024);
-          ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          for (int k = 0; k < gemm::BK / 16; ++k) {
+            const uint64_t ad = ptx::make_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = ptx::make_desc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          ptx::mma_commit(&empty[stage]);
         }
-        ptx::mma_commit(&empty[stage]);
+        __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-      ptx::mma_commit(&tmem_full[acc]);
+      if (leader) ptx::mma_commit(&tmem_full[acc]);
+      __syncwarp();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
@@ -163,6 +173,7 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
     const int wq = warp & 3;    // TMEM lane quadrant this warp may access
     const int half = ew >> 2;   // which interleaved half of the 32-column chunks
     uint8_t* box = smem_box + ew * gemm::kBoxBytes;
+    const bool epi_leader = ptx::elect_one();  // same lane issues stores and waits (bulk groups are per thread)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
@@ -186,12 +197,12 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         epilogue_math<EPI, 32, true>(v, ep, g, row, col0);
-        if (lane == 0) ptx::tma_store_wait_read<0>();  // staging box free again
+        if (epi_leader) ptx::tma_store_wait_read<0>();  // staging box free again
         __syncwarp();
         stage_row32<kF32>(box, lane, v);
         ptx::fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
+        if (epi_leader) {
           ptx::tma_store_3d(&tmO, box, ep.out_col0 + col0, row0, g);
           ptx::tma_store_commit();
         }
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
       if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (lane == 0) ptx::tma_store_wait<0>();
+    if (epi_leader) ptx::tma_store_wait<0>();
     __syncwarp();
   }
 
