@@ -58,7 +58,27 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], const GemmEpilogue
 #pragma unroll
     for (int j = 0; j < NV; ++j) v[j] = gelu_tanh<kFastMath>(v[j]);
   }
-  if constexpr (kResid) {
+  if constexpr (kResid && (EPI & 256) != 0) {
+    // bf16 residual (EPI_RESID_BF16): 8 values per 16-byte load
+    const __nv_bfloat16* rp = ep.resid_b + g * ep.resid_gstride + static_cast<long long>(row) * ep.resid_ld + col0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < NV; j += 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(rp + j);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(h2[q]);
+          v[j + 2 * q] += f.x;
+          v[j + 2 * q + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (col0 + j < ep.N) v[j] += __bfloat162float(rp[j]);
+    }
+  } else if constexpr (kResid) {
     const float* rp = ep.resid + g * ep.resid_gstride + static_cast<long long>(row) * ep.resid_ld + col0;
     if (full) {
 #pragma unroll

@@ -64,6 +64,11 @@ struct LayerW {
   float* ln1_b = nullptr;
   float* ln2_g = nullptr;
   float* ln2_b = nullptr;  // [G][D]
+  // bf16 path (folded LayerNorm): Wqkv / W1 hold gamma-scaled rows; these are
+  // the column biases beta @ W (+ b1 for W1)
+  float* cqkv = nullptr;  // [G][3DA]
+  float* c1 = nullptr;    // [G][F]
+  float* u1 = nullptr;    // [G][F] ln2_scale @ w1 (mean correction of the folded LN2)
 };
 
 }  // namespace
@@ -82,6 +87,7 @@ struct FlameCtx {
   void* we1 = nullptr;      // [F][D]
   float* be1 = nullptr;     // [F]
   float* we2 = nullptr;     // [F][tasks]
+  float* we2p = nullptr;    // [F][4] tasks zero-padded to 4 (fused expert epilogue)
   float* be2 = nullptr;     // [tasks]
   float* scale = nullptr;       // [G] 1/(tau sqrt(dh))
   float* scale_log2 = nullptr;  // [G] log2(e)/(tau sqrt(dh))
@@ -118,6 +124,14 @@ struct FlameExec {
   float* Xb = nullptr;
   void* Fz = nullptr;
   void* He = nullptr;
+  void* Ehc = nullptr;         // bf16 path: centered history rows [G][Rh][D]
+  void* Ecc = nullptr;         // bf16 path: centered candidate rows [Rc][D]
+  float* rs_h = nullptr;       // rstd of the history rows [G][Rh]
+  float* rs_c = nullptr;       // rstd of the candidate rows [Rc]
+  float* RS = nullptr;         // rstd of centered rows of later LayerNorms [G][rows]
+  float* partial = nullptr;    // expert row-dot partials [Rc][n_parts][tasks]
+  float* STATS = nullptr;      // folded LN2: per-row (sum, sumsq) partials [G][rows][stat_parts][2]
+  int stat_parts = 0;
   int* spos = nullptr;
   int* ustart = nullptr;
   long long* unique_ws = nullptr;
@@ -177,6 +191,27 @@ void pack_transposed(std::vector<T>& dst, size_t dst_off, int rows_pad, int cols
       dst[dst_off + static_cast<size_t>(out_map[n]) * cols_pad + in_map[k]] = cvt<T>(src[static_cast<size_t>(k) * n_out + n]);
 }
 
+// Folded LayerNorm (bf16 path): LN(x) W = rstd * ((x - mean) (gamma . W)) + beta W.
+// dst gets gamma[k] * W[k][n] (scaled in double, then rounded once); colbias[out_map[n]]
+// accumulates sum_k beta[k] W[k][n].
+template <typename T>
+void pack_transposed_folded(std::vector<T>& dst, size_t dst_off, int cols_pad, const double* src,
+                            int k_in, int n_out, const std::vector<int>& out_map,
+                            const std::vector<int>& in_map, const double* gamma, const double* beta,
+                            float* colbias, float* colsum = nullptr) {
+  for (int n = 0; n < n_out; ++n) {
+    double cb = 0.0, cs = 0.0;
+    for (int k = 0; k < k_in; ++k) {
+      const double wv = src[static_cast<size_t>(k) * n_out + n];
+      dst[dst_off + static_cast<size_t>(out_map[n]) * cols_pad + in_map[k]] = cvt<T>(wv * gamma[k]);
+      cb += beta[k] * wv;
+      cs += gamma[k] * wv;
+    }
+    colbias[out_map[n]] += static_cast<float>(cb);
+    if (colsum) colsum[out_map[n]] = static_cast<float>(cs);
+  }
+}
+
 template <typename T>
 int upload_weights(FlameCtx* c, const double* w, long long n_values) {
   const int d = c->d, f = c->f, G = c->G, L = c->L, D = c->D, DA = c->DA, F = c->F, dh = c->dh,
@@ -187,12 +222,16 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
   for (int hh = 0; hh < nh; ++hh)
     for (int j = 0; j < dh; ++j) head_map[hh * dh + j] = hh * 64 + j;
   // per-layer host staging, all blocks stacked
+  constexpr bool kFold = std::is_same<T, __nv_bfloat16>::value;  // bf16 path folds LayerNorm
   struct HostLayer {
     std::vector<T> wqkv, wo, w1, w2;
-    std::vector<float> b1, b2, l1g, l1b, l2g, l2b;
+    std::vector<float> b1, b2, l1g, l1b, l2g, l2b, cqkv, c1, u1;
   };
   std::vector<HostLayer> hl(L);
   for (auto& h : hl) {
+    h.cqkv.assign(static_cast<size_t>(G) * 3 * DA, 0.f);
+    h.c1.assign(static_cast<size_t>(G) * F, 0.f);
+    h.u1.assign(static_cast<size_t>(G) * F, 0.f);
     h.wqkv.assign(static_cast<size_t>(G) * 3 * DA * D, cvt<T>(0.0));
     h.wo.assign(static_cast<size_t>(G) * D * DA, cvt<T>(0.0));
     h.w1.assign(static_cast<size_t>(G) * F * D, cvt<T>(0.0));
@@ -222,23 +261,42 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
     for (int l = 0; l < L; ++l) {
       HostLayer& h = hl[l];
       const size_t qkv_off = static_cast<size_t>(b) * 3 * DA * D;
-      if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_q)");
-      pack_transposed(h.wqkv, qkv_off, 3 * DA, D, a, d, d, qmap, id_d);
-      if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_k)");
-      pack_transposed(h.wqkv, qkv_off, 3 * DA, D, a, d, d, kmap, id_d);
-      if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_v)");
-      pack_transposed(h.wqkv, qkv_off, 3 * DA, D, a, d, d, vmap, id_d);
-      if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_o)");
-      pack_transposed(h.wo, static_cast<size_t>(b) * D * DA, D, DA, a, d, d, id_d, head_map);
+      // stream order (params.py:116-121): w_q w_k w_v w_o ln1_scale ln1_shift
+      // ln2_scale ln2_shift w1 b1 w2 b2; the LN vectors follow the weights they fold into
+      const double* wsrc[4];
+      for (int q = 0; q < 4; ++q) {
+        if (!need(static_cast<long long>(d) * d)) return fail(1, "weights too short (w_q/k/v/o)");
+        wsrc[q] = a;
+      }
+      const double* lnsrc[4];
       float* lnv[4] = {h.l1g.data(), h.l1b.data(), h.l2g.data(), h.l2b.data()};
       for (int q = 0; q < 4; ++q) {
         if (!need(d)) return fail(1, "weights too short (ln)");
+        lnsrc[q] = a;
         for (int i = 0; i < d; ++i) lnv[q][static_cast<size_t>(b) * D + i] = static_cast<float>(a[i]);
       }
+      const std::vector<int>* maps[3] = {&qmap, &kmap, &vmap};
+      for (int q = 0; q < 3; ++q) {
+        if (kFold)
+          pack_transposed_folded(h.wqkv, qkv_off, D, wsrc[q], d, d, *maps[q], id_d, lnsrc[0], lnsrc[1],
+                                 h.cqkv.data() + static_cast<size_t>(b) * 3 * DA);
+        else
+          pack_transposed(h.wqkv, qkv_off, 3 * DA, D, wsrc[q], d, d, *maps[q], id_d);
+      }
+      pack_transposed(h.wo, static_cast<size_t>(b) * D * DA, D, DA, wsrc[3], d, d, id_d, head_map);
       if (!need(static_cast<long long>(d) * f)) return fail(1, "weights too short (w1)");
-      pack_transposed(h.w1, static_cast<size_t>(b) * F * D, F, D, a, d, f, id_f, id_d);
+      const double* w1src = a;
       if (!need(f)) return fail(1, "weights too short (b1)");
       for (int i = 0; i < f; ++i) h.b1[static_cast<size_t>(b) * F + i] = static_cast<float>(a[i]);
+      if (kFold) {
+        // c1 = ln2_shift @ w1 + b1 (the GELU input bias of the folded LN2 -> W1 GEMM)
+        float* c1 = h.c1.data() + static_cast<size_t>(b) * F;
+        for (int i = 0; i < f; ++i) c1[i] = static_cast<float>(a[i]);
+        pack_transposed_folded(h.w1, static_cast<size_t>(b) * F * D, D, w1src, d, f, id_f, id_d, lnsrc[2],
+                               lnsrc[3], c1, h.u1.data() + static_cast<size_t>(b) * F);
+      } else {
+        pack_transposed(h.w1, static_cast<size_t>(b) * F * D, F, D, w1src, d, f, id_f, id_d);
+      }
       if (!need(static_cast<long long>(f) * d)) return fail(1, "weights too short (w2)");
       pack_transposed(h.w2, static_cast<size_t>(b) * D * F, D, F, a, f, d, id_d, id_f);
       if (!need(d)) return fail(1, "weights too short (b2)");
@@ -281,6 +339,9 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
   if (!need(static_cast<long long>(f) * tasks)) return fail(1, "weights too short (expert_w2)");
   for (int k = 0; k < f; ++k)
     for (int t = 0; t < tasks; ++t) we2[static_cast<size_t>(k) * tasks + t] = static_cast<float>(a[static_cast<size_t>(k) * tasks + t]);
+  std::vector<float> we2p(static_cast<size_t>(F) * 4, 0.f);
+  for (int k = 0; k < f; ++k)
+    for (int t = 0; t < tasks && t < 4; ++t) we2p[static_cast<size_t>(k) * 4 + t] = we2[static_cast<size_t>(k) * tasks + t];
   if (!need(tasks)) return fail(1, "weights too short (expert_b2)");
   for (int t = 0; t < tasks; ++t) be2[t] = static_cast<float>(a[t]);
   if (cur.left != 0) return fail(1, "trailing values in weight stream (" + std::to_string(cur.left) + ")");
@@ -300,13 +361,15 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
     T *wqkv, *wo, *w1, *w2;
     if (!up(h.wqkv, &wqkv) || !up(h.wo, &wo) || !up(h.w1, &w1) || !up(h.w2, &w2) ||
         !up(h.b1, &lw.b1) || !up(h.b2, &lw.b2) || !up(h.l1g, &lw.ln1_g) || !up(h.l1b, &lw.ln1_b) ||
-        !up(h.l2g, &lw.ln2_g) || !up(h.l2b, &lw.ln2_b))
+        !up(h.l2g, &lw.ln2_g) || !up(h.l2b, &lw.ln2_b) || !up(h.cqkv, &lw.cqkv) || !up(h.c1, &lw.c1) ||
+        !up(h.u1, &lw.u1))
       return fail(2, "device allocation / copy of layer weights failed");
     lw.wqkv = wqkv; lw.wo = wo; lw.w1 = w1; lw.w2 = w2;
   }
   T* we1d;
   if (!up(gate_w, &c->gate_w) || !up(gate_b, &c->gate_b) || !up(we1, &we1d) || !up(be1, &c->be1) ||
-      !up(we2, &c->we2) || !up(be2, &c->be2) || !up(scale, &c->scale) || !up(scale_log2, &c->scale_log2))
+      !up(we2, &c->we2) || !up(we2p, &c->we2p) || !up(be2, &c->be2) || !up(scale, &c->scale) ||
+      !up(scale_log2, &c->scale_log2))
     return fail(2, "device allocation / copy of model weights failed");
   c->we1 = we1d;
   return 0;
@@ -370,6 +433,14 @@ struct Pipe {
   }
 
   const char* gemm_name = "gemm";
+  // extra epilogue operands for the next gemm() call (reset after it)
+  const float* rs_ptr = nullptr;
+  long long rs_g = 0;
+  const float* dot_w = nullptr;
+  int dot_n = 0;
+  double flop_div = 1.0;  // split-bf16 GEMMs do 3x the algorithmic FLOPs
+  GemmEpilogue ln{};      // folded-LN2 producer / consumer operands (reset after use)
+  const __nv_bfloat16* resid_b = nullptr;  // bf16 residual of the next gemm()
   int gemm(const Act* A, long long lda, long long a_gstride, int a_shared, const Act* W, long long ldw,
            long long w_gstride, int M, int N, int K, int G, void* out, long long out_ld,
            long long out_gstride, int out_col0, const float* bias, long long bias_gstride,
@@ -379,13 +450,21 @@ struct Pipe {
     ep.bias = bias; ep.bias_gstride = bias_gstride;
     ep.resid = resid; ep.resid_ld = resid_ld; ep.resid_gstride = resid_gstride;
     ep.M = M; ep.N = N;
+    ep.rowscale = rs_ptr; ep.rowscale_gstride = rs_g; ep.dot_w = dot_w; ep.dot_n = dot_n;
+    ep.out2 = ln.out2; ep.out2_ld = ln.out2_ld; ep.out2_gstride = ln.out2_gstride;
+    ep.stats = ln.stats; ep.stats_gstride = ln.stats_gstride;
+    ep.lnstats = ln.lnstats; ep.lnstats_gstride = ln.lnstats_gstride; ep.stats_parts = ln.stats_parts;
+    ep.d_true = ln.d_true; ep.colsum = ln.colsum; ep.colsum_gstride = ln.colsum_gstride;
+    ep.resid_b = resid_b;
+    rs_ptr = nullptr; rs_g = 0; dot_w = nullptr; dot_n = 0; ln = GemmEpilogue{}; resid_b = nullptr;
     if (M <= 0) return 0;
     {
       const double ab = sizeof(Act);
       const double ob = (epi & EPI_OUT_F32) || !std::is_same<Act, __nv_bfloat16>::value ? 4.0 : 2.0;
       const double byts = static_cast<double>(G) * (static_cast<double>(M) * K * ab + static_cast<double>(N) * K * ab +
                                                     static_cast<double>(M) * N * (ob + ((epi & EPI_RESID) ? 4.0 : 0.0)));
-      mark(gemm_name, 2.0 * G * static_cast<double>(M) * N * K, byts);
+      mark(gemm_name, 2.0 * G * static_cast<double>(M) * N * K / flop_div, byts);
+      flop_div = 1.0;
     }
     if constexpr (std::is_same<Act, __nv_bfloat16>::value) {
       GemmProblem p{};
@@ -478,15 +557,27 @@ struct Pipe {
     return check();
   }
 
+  AssembleOut assemble_out() const {
+    AssembleOut o{};
+    o.Eh = e->Eh;  // null unless needed (history residual of L >= 2, fp32 mode)
+    o.Ec = e->Ec;
+    o.Ehc = static_cast<__nv_bfloat16*>(e->Ehc);
+    o.Ecc = static_cast<__nv_bfloat16*>(e->Ecc);
+    o.rs_h = e->rs_h;
+    o.rs_c = e->rs_c;
+    return o;
+  }
+
   int assemble(int mode) {
+    const double row_bytes = (e->Eh ? 4.0 : 0.0) + (e->Ehc ? 2.0 : 0.0);
     if (mode == FLAME_INPUT_EMBEDDINGS) {
       if (!e->io.hist_emb || !e->io.cand_emb) return fail(1, "embedding inputs not bound");
       const long long warps = static_cast<long long>(c->G) * e->Rh + e->Rc;
       const int threads = 256;
-      mark("scatter_embeddings", 0.0, static_cast<double>(warps) * (c->d + c->D) * 4.0);
+      mark("scatter_embeddings", 0.0, static_cast<double>(warps) * (c->d * 4.0 + c->D * (row_bytes + 4.0)));
       scatter_embeddings<<<static_cast<unsigned>((warps * 32 + threads - 1) / threads), threads, 0, s>>>(
           e->io.hist_emb, e->io.cand_emb, c->d, c->D, e->R, e->H_bkt, e->c_bkt, c->G, e->hb_bkt,
-          e->io.hist_len, e->io.cand_len, e->Eh, e->Ec);
+          e->io.hist_len, e->io.cand_len, assemble_out());
       return check();
     }
     if (!e->io.hist_ids || !e->io.cand_ids) return fail(1, "id inputs not bound");
@@ -512,16 +603,17 @@ struct Pipe {
     if (int rc = check()) return rc;
     {
       PdaGatherArgs g{};
-      g.l = l; g.table = c->table; g.num_items = c->num_items; g.D = c->D; g.G = c->G;
-      g.hb_bkt = e->hb_bkt; g.Eh = e->Eh; g.Ec = e->Ec;
+      g.l = l; g.table = c->table; g.num_items = c->num_items; g.D = c->D; g.d_true = c->d; g.G = c->G;
+      g.hb_bkt = e->hb_bkt; g.o = assemble_out();
       int bx = (c->num_sms * 8 + 2 * e->R - 1) / (2 * e->R);
       if (bx < 1) bx = 1;
       const int max_bx = (e->cap + 7) / 8;
       if (bx > max_bx) bx = max_bx < 1 ? 1 : max_bx;
       dim3 grid(bx, 2 * e->R);
-      // rows out (fp32) + table rows read (upper bound: one per position)
-      mark("pda_gather", 0.0, static_cast<double>(e->R) * (e->H_bkt + e->c_bkt) * c->D *
-                                  (4.0 + (c->table_dtype == FLAME_TABLE_BF16 ? 2.0 : 4.0)));
+      // rows out + table rows read (upper bound: one per position); candidates also get fp32
+      const double tab = c->table_dtype == FLAME_TABLE_BF16 ? 2.0 : 4.0;
+      mark("pda_gather", 0.0, static_cast<double>(e->R) * c->D *
+                                  (e->H_bkt * (tab + row_bytes) + e->c_bkt * (tab + 4.0 + (e->Ecc ? 2.0 : 0.0))));
       if (c->table_dtype == FLAME_TABLE_BF16)
         pda_gather<__nv_bfloat16><<<grid, 256, 0, s>>>(g);
       else
@@ -531,9 +623,26 @@ struct Pipe {
     return 0;
   }
 
+  // fp32 rows -> centered bf16 rows + rstd (folded LayerNorm input)
+  int center(const float* src, long long src_gstride, Act* out, long long out_gstride, float* rs,
+             long long rs_gstride, long long rows) {
+    if (rows <= 0) return 0;
+    if constexpr (std::is_same<Act, __nv_bfloat16>::value) {
+      const int threads = 256;
+      dim3 grid(static_cast<unsigned>((rows * 32 + threads - 1) / threads), c->G);
+      mark("center_rows", 0.0, static_cast<double>(c->G) * rows * c->D * 6.0);
+      center_rows<<<grid, threads, 0, s>>>(src, c->D, src_gstride, out, c->D, out_gstride, rs, rs_gstride,
+                                           static_cast<int>(rows), c->D, c->d);
+      return check();
+    } else {
+      return fail(2, "center() is bf16-path only");
+    }
+  }
+
   int run(int mode) {
     if (int rc = assemble(mode)) return rc;
     if (mode == FLAME_INPUT_GATHER_ONLY) return 0;
+    constexpr bool kFold = std::is_same<Act, __nv_bfloat16>::value;  // folded LayerNorm path
     const int D = c->D, DA = c->DA, F = c->F, G = c->G;
     const long long rows = e->rows, Rh = e->Rh, Rc = e->Rc;
     const long long gD = rows * D, gQKV = rows * 3LL * DA, gA = rows * DA, gF = rows * F;
@@ -541,56 +650,107 @@ struct Pipe {
     Act* QKV = act(e->QKV);
     Act* AO = act(e->AO);
     Act* Hf = act(e->Hf);
+    float* RS = e->RS;
     float* Xcur = nullptr;  // residual stream input of this layer (null at layer 0)
     for (int l = 0; l < c->L; ++l) {
       const LayerW& w = c->layers[l];
       const bool last = l == c->L - 1;
-      // sources of this layer's input rows
+      // fp32 sources of this layer's input rows (residual / LN input)
       const float* src_h = l == 0 ? e->Eh : Xcur;
       const long long src_h_g = l == 0 ? Rh * D : gD;
       const float* src_c = l == 0 ? e->Ec : Xcur + Rh * D;
       const long long src_c_g = l == 0 ? 0 : gD;
       float* Xnext = (Xcur == e->Xa) ? e->Xb : e->Xa;
-      // LN1 (forward.py:111 / :120)
-      if (int rc = layer_norm(src_h, D, src_h_g, Y, D, gD, w.ln1_g, w.ln1_b, Rh)) return rc;
-      if (int rc = layer_norm(src_c, D, src_c_g, Y + Rh * D, D, gD, w.ln1_g, w.ln1_b, Rc)) return rc;
+      // LN1 (forward.py:111 / :120): GEMM A operands (+ folded row scales)
+      const Act *A_h, *A_c;
+      long long A_h_g, A_c_g;
+      int A_c_shared = 0;
+      const float *rs_h = nullptr, *rs_c = nullptr;
+      long long rs_h_g = 0, rs_c_g = 0;
+      if constexpr (kFold) {
+        if (l == 0) {
+          // centered rows + rstd come straight from the feature assembly; the
+          // candidate statistics are shared by every block
+          A_h = static_cast<const Act*>(e->Ehc); A_h_g = Rh * D; rs_h = e->rs_h; rs_h_g = Rh;
+          A_c = static_cast<const Act*>(e->Ecc); A_c_g = 0; A_c_shared = 1; rs_c = e->rs_c; rs_c_g = 0;
+        } else {
+          if (int rc = center(src_h, gD, Y, gD, RS, rows, Rh)) return rc;
+          if (int rc = center(src_c, gD, Y + Rh * D, gD, RS + Rh, rows, Rc)) return rc;
+          A_h = Y; A_h_g = gD; rs_h = RS; rs_h_g = rows;
+          A_c = Y + Rh * D; A_c_g = gD; rs_c = RS + Rh; rs_c_g = rows;
+        }
+      } else {
+        if (int rc = layer_norm(src_h, D, src_h_g, Y, D, gD, w.ln1_g, w.ln1_b, Rh)) return rc;
+        if (int rc = layer_norm(src_c, D, src_c_g, Y + Rh * D, D, gD, w.ln1_g, w.ln1_b, Rc)) return rc;
+        A_h = Y; A_h_g = gD; A_c = Y + Rh * D; A_c_g = gD;
+      }
+      const int qkv_epi = kFold ? (EPI_ROWSCALE | EPI_BIAS) : 0;
       // projections (forward.py:112-114 last layer: history rows K,V only; :121-123 others)
       const Act* Wqkv = act(w.wqkv);
+      rs_ptr = rs_h; rs_g = rs_h_g;
       if (last) {
         gemm_name = "gemm_kv_hist";
-        if (int rc = gemm(Y, D, gD, 0, Wqkv + static_cast<long long>(DA) * D, D, 3LL * DA * D, Rh, 2 * DA, D, G,
-                          QKV, 3LL * DA, gQKV, DA, nullptr, 0, nullptr, 0, 0, 0)) return rc;
+        if (int rc = gemm(A_h, D, A_h_g, 0, Wqkv + static_cast<long long>(DA) * D, D, 3LL * DA * D, Rh, 2 * DA, D, G,
+                          QKV, 3LL * DA, gQKV, DA, w.cqkv + DA, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
       } else {
         gemm_name = "gemm_qkv_hist";
-        if (int rc = gemm(Y, D, gD, 0, Wqkv, D, 3LL * DA * D, Rh, 3 * DA, D, G, QKV, 3LL * DA, gQKV, 0,
-                          nullptr, 0, nullptr, 0, 0, 0)) return rc;
+        if (int rc = gemm(A_h, D, A_h_g, 0, Wqkv, D, 3LL * DA * D, Rh, 3 * DA, D, G, QKV, 3LL * DA, gQKV, 0,
+                          w.cqkv, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
       }
+      rs_ptr = rs_c; rs_g = rs_c_g;
       gemm_name = "gemm_qkv_cand";
-      if (int rc = gemm(Y + Rh * D, D, gD, 0, Wqkv, D, 3LL * DA * D, Rc, 3 * DA, D, G, QKV + Rh * 3LL * DA,
-                        3LL * DA, gQKV, 0, nullptr, 0, nullptr, 0, 0, 0)) return rc;
+      if (int rc = gemm(A_c, D, A_c_g, A_c_shared, Wqkv, D, 3LL * DA * D, Rc, 3 * DA, D, G, QKV + Rh * 3LL * DA,
+                        3LL * DA, gQKV, 0, w.cqkv, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
       // SUMI attention (attention.py:118-146; :149-178 for non-final layers)
       if (int rc = attention(false)) return rc;
       if (!last) { if (int rc = attention(true)) return rc; }
       // O-projection + residual (forward.py:116 / :135)
+      // bf16 path: X1 is written once in bf16 (it is both the W1 A operand and the
+      // W2 residual) together with per-row (sum, sumsq) partials, so LN2 needs
+      // no pass of its own; fp32 path: fp32 X1 + explicit LayerNorm
+      const long long SP = static_cast<long long>(e->stat_parts) * 2;  // floats per row
+      void* X1 = kFold ? static_cast<void*>(Y) : static_cast<void*>(e->X1);
+      auto ln_producer = [&](long long r0) {
+        if (!kFold) return;
+        ln.stats = e->STATS + r0 * SP; ln.stats_gstride = rows * SP;
+      };
+      const int oproj_epi = kFold ? (EPI_RESID | EPI_STATS) : (EPI_RESID | EPI_OUT_F32);
+      const long long esz = kFold ? 2 : 4;
       gemm_name = "gemm_oproj_cand";
+      ln_producer(Rh);
       if (int rc = gemm(AO + Rh * DA, DA, gA, 0, act(w.wo), DA, static_cast<long long>(D) * DA, Rc, D, DA, G,
-                        e->X1 + Rh * D, D, gD, 0, nullptr, 0, src_c, D, src_c_g, EPI_RESID | EPI_OUT_F32)) return rc;
+                        static_cast<char*>(X1) + Rh * D * esz, D, gD, 0, nullptr, 0, src_c, D, src_c_g, oproj_epi)) return rc;
       if (!last) {
         gemm_name = "gemm_oproj_hist";
-        if (int rc = gemm(AO, DA, gA, 0, act(w.wo), DA, static_cast<long long>(D) * DA, Rh, D, DA, G, e->X1, D, gD, 0,
-                          nullptr, 0, src_h, D, src_h_g, EPI_RESID | EPI_OUT_F32)) return rc;
+        ln_producer(0);
+        if (int rc = gemm(AO, DA, gA, 0, act(w.wo), DA, static_cast<long long>(D) * DA, Rh, D, DA, G, X1, D, gD, 0,
+                          nullptr, 0, src_h, D, src_h_g, oproj_epi)) return rc;
       }
       // LN2 + FFN + residual (forward.py:117-118 / :137-138)
       const long long r0 = last ? Rh : 0;  // first row of the range that continues
       const long long nr = last ? Rc : rows;
-      if (int rc = layer_norm(e->X1 + r0 * D, D, gD, Y + r0 * D, D, gD, w.ln2_g, w.ln2_b, nr)) return rc;
       gemm_name = "gemm_ffn_w1";
-      if (int rc = gemm(Y + r0 * D, D, gD, 0, act(w.w1), D, static_cast<long long>(F) * D, static_cast<int>(nr), F, D, G,
-                        Hf + r0 * F, F, gF, 0, w.b1, F, nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
+      if constexpr (kFold) {
+        ln.lnstats = e->STATS + r0 * SP; ln.lnstats_gstride = rows * SP; ln.stats_parts = e->stat_parts;
+        ln.d_true = c->d; ln.colsum = w.u1; ln.colsum_gstride = F;
+        if (int rc = gemm(Y + r0 * D, D, gD, 0, act(w.w1), D, static_cast<long long>(F) * D, static_cast<int>(nr), F, D, G,
+                          Hf + r0 * F, F, gF, 0, w.c1, F, nullptr, 0, 0, EPI_LNSTATS | EPI_BIAS | EPI_GELU)) return rc;
+      } else {
+        if (int rc = layer_norm(e->X1 + r0 * D, D, gD, Y + r0 * D, D, gD, w.ln2_g, w.ln2_b, nr)) return rc;
+        if (int rc = gemm(Y + r0 * D, D, gD, 0, act(w.w1), D, static_cast<long long>(F) * D, static_cast<int>(nr), F, D, G,
+                          Hf + r0 * F, F, gF, 0, w.b1, F, nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
+      }
       gemm_name = "gemm_ffn_w2";
-      if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F, G,
-                        Xnext + r0 * D, D, gD, 0, w.b2, D, e->X1 + r0 * D, D, gD,
-                        EPI_BIAS | EPI_RESID | EPI_OUT_F32)) return rc;
+      if constexpr (kFold) {
+        resid_b = reinterpret_cast<const __nv_bfloat16*>(Y) + r0 * D;
+        if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F,
+                          G, Xnext + r0 * D, D, gD, 0, w.b2, D, nullptr, D, gD,
+                          EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32)) return rc;
+      } else {
+        if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F,
+                          G, Xnext + r0 * D, D, gD, 0, w.b2, D, e->X1 + r0 * D, D, gD,
+                          EPI_BIAS | EPI_RESID | EPI_OUT_F32)) return rc;
+      }
       Xcur = Xnext;
     }
     // gated fusion over blocks (forward.py:143-156)
@@ -603,15 +763,29 @@ struct Pipe {
     }
     // expert heads (forward.py:159-166)
     gemm_name = "gemm_expert_w1";
-    // split-bf16 (bf16 mode): K = 3D over [Fz_hi|Fz_hi|Fz_lo] x [W_hi|W_lo|W_hi]; He kept fp32
-    if (int rc = gemm(act(e->Fz), kSplitK * D, 0, 1, act(c->we1), kSplitK * D, 0, static_cast<int>(Rc), F, kSplitK * D, 1,
-                      e->He, F, 0, 0, c->be1, 0, nullptr, 0, 0, EPI_BIAS | EPI_GELU | EPI_OUT_F32)) return rc;
-    {
+    if (kFold && c->tasks <= 4) {
+      // split-bf16 K = 3D over [Fz_hi|Fz_hi|Fz_lo] x [W_hi|W_lo|W_hi]; the epilogue applies
+      // bias + GELU and dots each row with expert_w2, so the hidden layer never reaches HBM
+      dot_w = c->we2p; dot_n = c->tasks; flop_div = 3.0;
+      if (int rc = gemm(act(e->Fz), kSplitK * D, 0, 1, act(c->we1), kSplitK * D, 0, static_cast<int>(Rc), F,
+                        kSplitK * D, 1, e->partial, 0, 0, 0, c->be1, 0, nullptr, 0, 0,
+                        EPI_BIAS | EPI_GELU | EPI_ROWDOT)) return rc;
+      const int n_parts = gemm_row_parts(F, EPI_BIAS | EPI_GELU | EPI_ROWDOT);
+      mark("expert_combine", 0.0, static_cast<double>(Rc) * n_parts * c->tasks * 4.0);
+      expert_combine<<<static_cast<unsigned>((Rc + 255) / 256), 256, 0, s>>>(
+          e->partial, n_parts, c->tasks, c->be2, e->c_bkt, e->io.cand_len, e->io.out_offset, e->io.scores,
+          static_cast<int>(Rc));
+      if (int rc = check()) return rc;
+    } else {
+      flop_div = kSplitK;
+      if (int rc = gemm(act(e->Fz), kSplitK * D, 0, 1, act(c->we1), kSplitK * D, 0, static_cast<int>(Rc), F,
+                        kSplitK * D, 1, e->He, F, 0, 0, c->be1, 0, nullptr, 0, 0, EPI_BIAS | EPI_GELU | EPI_OUT_F32))
+        return rc;
       const long long threads = Rc * 32;
       mark("expert_out", 2.0 * Rc * F * c->tasks, static_cast<double>(Rc) * F * 4.0);
       expert_out_rows<float><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
-          static_cast<const float*>(e->He), F, c->we2, c->be2, F, c->tasks, e->c_bkt, e->io.cand_len, e->io.out_offset,
-          e->io.scores, static_cast<int>(Rc));
+          static_cast<const float*>(e->He), F, c->we2, c->be2, F, c->tasks, e->c_bkt, e->io.cand_len,
+          e->io.out_offset, e->io.scores, static_cast<int>(Rc));
       if (int rc = check()) return rc;
     }
     return 0;
@@ -765,17 +939,30 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
     ok = ok && p != nullptr;
     return p;
   };
-  e->Eh = static_cast<float*>(A(G * e->Rh * D * 4));
+  const bool fold = c->precision == FLAME_BF16;  // folded-LayerNorm bf16 path
+  // fp32 history rows are only needed as a residual (L >= 2) or as LN input (fp32 mode)
+  e->Eh = (!fold || c->L > 1) ? static_cast<float*>(A(G * e->Rh * D * 4)) : nullptr;
   e->Ec = static_cast<float*>(A(e->Rc * D * 4));
+  if (fold) {
+    e->Ehc = A(G * e->Rh * D * 2);
+    e->Ecc = A(e->Rc * D * 2);
+    e->rs_h = static_cast<float*>(A(G * e->Rh * 4));
+    e->rs_c = static_cast<float*>(A(e->Rc * 4));
+    e->RS = static_cast<float*>(A(G * rows * 4));
+    e->stat_parts = gemm_row_parts(D, EPI_RESID | EPI_OUT_F32 | EPI_STATS);
+    e->STATS = static_cast<float*>(A(G * rows * e->stat_parts * 2 * 4));
+    const size_t n_parts = gemm_row_parts(F, EPI_BIAS | EPI_GELU | EPI_ROWDOT);
+    if (c->tasks <= 4) e->partial = static_cast<float*>(A(e->Rc * n_parts * c->tasks * 4));
+  }
   e->Y = A(G * rows * D * ab);
   e->QKV = A(G * rows * 3 * DA * ab);
   e->AO = A(G * rows * DA * ab);
-  e->X1 = static_cast<float*>(A(G * rows * D * 4));
+  e->X1 = fold ? nullptr : static_cast<float*>(A(G * rows * D * 4));
   e->Hf = A(G * rows * F * ab);
   e->Xa = static_cast<float*>(A(G * rows * D * 4));
   e->Xb = c->L > 1 ? static_cast<float*>(A(G * rows * D * 4)) : nullptr;
-  e->Fz = A(e->Rc * D * ab * (c->precision == FLAME_BF16 ? 3 : 1));
-  e->He = A(e->Rc * F * 4);
+  e->Fz = A(e->Rc * D * ab * (fold ? 3 : 1));
+  e->He = (fold && c->tasks <= 4) ? nullptr : A(e->Rc * F * 4);
   e->spos = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
   e->ustart = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
   e->unique_ws = static_cast<long long*>(A(2 * static_cast<size_t>(R) * cap * 8));

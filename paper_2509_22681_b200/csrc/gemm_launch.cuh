@@ -21,7 +21,7 @@ struct GemmProblem {
 
 template <int BN, int EPI>
 static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_sms) {
-  using C = gemm::Cfg<BN>;
+  using C = gemm::Cfg<BN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, EPI>,
@@ -37,9 +37,18 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
     return cudaErrorInvalidValue;
   CUtensorMap to;
   constexpr int ob = (EPI & EPI_OUT_F32) ? 4 : 2;
-  if (!make_tmap_out_3d(&to, p.ep.out, ob, static_cast<uint64_t>(p.ep.out_col0) + p.N, p.M, p.G,
-                        p.ep.out_ld * ob, p.ep.out_gstride * ob))
+  if constexpr ((EPI & EPI_ROWDOT) != 0) {
+    // row-dot epilogue writes its partials directly; the map is a valid placeholder
+    if (!make_tmap_out_3d(&to, p.ep.out, 4, 32, p.M, 1, 128, 0)) return cudaErrorInvalidValue;
+  } else if (!make_tmap_out_3d(&to, p.ep.out, ob, static_cast<uint64_t>(p.ep.out_col0) + p.N, p.M, p.G,
+                               p.ep.out_ld * ob, p.ep.out_gstride * ob)) {
     return cudaErrorInvalidValue;
+  }
+  CUtensorMap to2 = to;
+  if constexpr (C::kDual) {
+    if (!make_tmap_out_3d(&to2, p.ep.out2, 2, p.N, p.M, p.G, p.ep.out2_ld * 2, p.ep.out2_gstride * 2))
+      return cudaErrorInvalidValue;
+  }
   const int m_tiles = (p.M + gemm::BM - 1) / gemm::BM;
   const int n_tiles = (p.N + BN - 1) / BN;
   const int total = p.G * m_tiles * n_tiles;
@@ -47,8 +56,8 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   GemmEpilogue ep = p.ep;
   ep.M = p.M;
   ep.N = p.N;
-  gemm_bf16_tcgen05<BN, EPI><<<grid, gemm::kThreads, C::kSmemBytes, s>>>(
-      ta, tb, to, p.K / gemm::BK, m_tiles, n_tiles, p.G, p.a_shared, ep);
+  gemm_bf16_tcgen05<BN, EPI><<<grid, C::kThreads, C::kSmemBytes, s>>>(
+      ta, tb, to, to2, p.K / gemm::BK, m_tiles, n_tiles, p.G, p.a_shared, ep);
   return cudaGetLastError();
 }
 
@@ -64,8 +73,28 @@ static cudaError_t launch_gemm_bn(const GemmProblem& p, cudaStream_t s, int num_
       return launch_gemm_t<BN, EPI_BIAS | EPI_RESID | EPI_OUT_F32>(p, s, num_sms);
     case EPI_BIAS | EPI_GELU | EPI_OUT_F32:
       return launch_gemm_t<BN, EPI_BIAS | EPI_GELU | EPI_OUT_F32>(p, s, num_sms);
+    case EPI_ROWSCALE | EPI_BIAS: return launch_gemm_t<BN, EPI_ROWSCALE | EPI_BIAS>(p, s, num_sms);
+    case EPI_ROWSCALE | EPI_BIAS | EPI_GELU:
+      return launch_gemm_t<BN, EPI_ROWSCALE | EPI_BIAS | EPI_GELU>(p, s, num_sms);
+    case EPI_RESID | EPI_OUT_F32 | EPI_STATS:
+      return launch_gemm_t<BN, EPI_RESID | EPI_OUT_F32 | EPI_STATS>(p, s, num_sms);
+    case EPI_RESID | EPI_STATS: return launch_gemm_t<BN, EPI_RESID | EPI_STATS>(p, s, num_sms);
+    case EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32:
+      return launch_gemm_t<BN, EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32>(p, s, num_sms);
+    case EPI_LNSTATS | EPI_BIAS | EPI_GELU:
+      return launch_gemm_t<BN, EPI_LNSTATS | EPI_BIAS | EPI_GELU>(p, s, num_sms);
+    case EPI_BIAS | EPI_GELU | EPI_ROWDOT:
+      return launch_gemm_t<BN, EPI_BIAS | EPI_GELU | EPI_ROWDOT>(p, s, num_sms);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// Per-row partial count written by the STATS / ROWDOT epilogues of a GEMM with
+// N output columns: one per (column tile, epilogue-warp share).
+static int gemm_row_parts(int N, int epi) {
+  const int bn = N >= 256 ? 256 : 128;
+  const bool heavy = (epi & (EPI_GELU | EPI_LNSTATS | EPI_STATS)) != 0;
+  return ((N + bn - 1) / bn) * (heavy ? 3 : 2);
 }
 
 static cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t s, int num_sms) {

@@ -145,12 +145,30 @@ struct PdaGatherArgs {
   PdaLists l;
   const void* table;  // [num_items][D] (bf16 or fp32), unknown ids -> zero rows
   long long num_items;
-  int D;
+  int D, d_true;
   int G;       // Climber blocks (history split)
   int hb_bkt;  // history rows per request-block in the row space
-  float* Eh;   // [G][R*hb_bkt][D]
-  float* Ec;   // [R*C_bkt][D]
+  AssembleOut o;  // fp32 rows (optional) + centered bf16 rows + rstd (folded LN1)
 };
+
+__device__ __forceinline__ void assemble_row_st(const AssembleOut& o, bool hist, long long row,
+                                                const float4 (&v)[8], int lane, int D, int d_true,
+                                                RowStats st) {
+  float* f = hist ? o.Eh : o.Ec;
+  if (f != nullptr) {
+    float* dst = f + row * D;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = (k * 32 + lane) * 4;
+      if (c < D) *reinterpret_cast<float4*>(dst + c) = v[k];
+    }
+  }
+  __nv_bfloat16* y = hist ? o.Ehc : o.Ecc;
+  if (y != nullptr) {
+    store_centered<8>(y + row * D, v, st.mean, lane, D, d_true);
+    if (lane == 0) (hist ? o.rs_h : o.rs_c)[row] = st.rstd;
+  }
+}
 
 template <typename TTab>
 __global__ void pda_gather(PdaGatherArgs a) {
@@ -168,6 +186,13 @@ __global__ void pda_gather(PdaGatherArgs a) {
   const int* us = a.l.ustart + static_cast<long long>(list) * a.l.cap;
   const TTab* table = reinterpret_cast<const TTab*>(a.table);
   const int hb = is_hist ? n / a.G : 0;
+  auto row_of = [&](int p) -> long long {  // destination row of list position p
+    if (is_hist) {
+      const int g = p / hb, i = p % hb;
+      return static_cast<long long>(g) * a.l.R * a.hb_bkt + static_cast<long long>(r) * a.hb_bkt + i;
+    }
+    return static_cast<long long>(r) * a.l.C_bkt + p;
+  };
   for (int u = wid; u < nu; u += warps_per_grid_x) {
     const long long id = uq[u];
     const bool known = id >= 0 && id < a.num_items;
@@ -177,36 +202,27 @@ __global__ void pda_gather(PdaGatherArgs a) {
       const int c = (k * 32 + lane) * 4;
       v[k] = (known && c < a.D) ? load_row4<TTab>(table + id * a.D, c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    // the row is read once; its LayerNorm statistics are computed once per unique id
+    const RowStats st = warp_row_stats<kMaxChunks>(v, lane, a.D, a.d_true);
     const int b = us[u];
     const int e = (u + 1 < nu) ? us[u + 1] : n;
-    for (int k = b; k < e; ++k) {
-      const int p = sp[k];
-      float* dst;
-      if (is_hist) {
-        const int g = p / hb, i = p % hb;
-        dst = a.Eh + (static_cast<long long>(g) * a.l.R * a.hb_bkt + static_cast<long long>(r) * a.hb_bkt + i) * a.D;
-      } else {
-        dst = a.Ec + (static_cast<long long>(r) * a.l.C_bkt + p) * a.D;
-      }
-#pragma unroll
-      for (int q = 0; q < kMaxChunks; ++q) {
-        const int c = (q * 32 + lane) * 4;
-        if (c < a.D) *reinterpret_cast<float4*>(dst + c) = v[q];
-      }
-    }
+    for (int k = b; k < e; ++k) assemble_row_st(a.o, is_hist, row_of(sp[k]), v, lane, a.D, a.d_true, st);
   }
   // zero the padding rows of this list's region (rows past the actual length)
   const int pad_rows = is_hist ? a.G * (a.hb_bkt - hb) : (a.l.C_bkt - n);
+  float4 z[kMaxChunks];
+#pragma unroll
+  for (int k = 0; k < kMaxChunks; ++k) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int k = wid; k < pad_rows; k += warps_per_grid_x) {
-    float* dst;
+    long long row;
     if (is_hist) {
       const int per = a.hb_bkt - hb;
       const int g = k / per, i = hb + k % per;
-      dst = a.Eh + (static_cast<long long>(g) * a.l.R * a.hb_bkt + static_cast<long long>(r) * a.hb_bkt + i) * a.D;
+      row = static_cast<long long>(g) * a.l.R * a.hb_bkt + static_cast<long long>(r) * a.hb_bkt + i;
     } else {
-      dst = a.Ec + (static_cast<long long>(r) * a.l.C_bkt + n + k) * a.D;
+      row = static_cast<long long>(r) * a.l.C_bkt + n + k;
     }
-    for (int c = lane * 4; c < a.D; c += 128) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    assemble_row_st(a.o, is_hist, row, z, lane, a.D, a.d_true, RowStats{0.f, 0.f});
   }
 }
 

@@ -156,15 +156,140 @@ __global__ void expert_out_rows(const TIn* __restrict__ hidden, long long h_ld,
   }
 }
 
+}  // namespace flame
+
+namespace flame {
+
+// ---------------------------------------------------------- folded LayerNorm
+// LN(x) W = rstd * ((x - mean) (gamma . W)) + beta W, so a row only needs its
+// centered values (bf16, padded columns 0) and rstd; gamma / beta live in the
+// folded weights and the GEMM epilogue (EPI_ROWSCALE | EPI_BIAS).  Statistics
+// follow reference forward.py:43-47 (biased variance of the deviations).
+struct RowStats {
+  float mean, rstd;
+};
+
+template <int kChunks>
+__device__ __forceinline__ RowStats warp_row_stats(const float4 (&v)[kChunks], int lane, int D,
+                                                   int d_true) {
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < kChunks; ++k) sum += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / d_true;
+  float sq = 0.f;
+#pragma unroll
+  for (int k = 0; k < kChunks; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    const float e[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (c + q < d_true) sq = fmaf(e[q] - mean, e[q] - mean, sq);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  (void)D;
+  return {mean, rsqrtf(sq / d_true + 1e-5f)};
+}
+
+template <int kChunks>
+__device__ __forceinline__ void store_centered(__nv_bfloat16* y, const float4 (&v)[kChunks], float mean,
+                                               int lane, int D, int d_true) {
+#pragma unroll
+  for (int k = 0; k < kChunks; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    if (c < D) {
+      const float a0 = c + 0 < d_true ? v[k].x - mean : 0.f;
+      const float a1 = c + 1 < d_true ? v[k].y - mean : 0.f;
+      const float a2 = c + 2 < d_true ? v[k].z - mean : 0.f;
+      const float a3 = c + 3 < d_true ? v[k].w - mean : 0.f;
+      store4<__nv_bfloat16>(y + c, a0, a1, a2, a3);
+    }
+  }
+}
+
+// fp32 rows -> centered bf16 rows + rstd (LN1 of layers > 0, LN2): one warp per row.
+__global__ void center_rows(const float* __restrict__ src, long long src_ld, long long src_gstride,
+                            __nv_bfloat16* __restrict__ out, long long out_ld, long long out_gstride,
+                            float* __restrict__ rstd, long long rs_gstride, int rows, int D, int d_true) {
+  constexpr int kChunks = 8;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const int g = blockIdx.y;
+  if (warp >= rows) return;
+  const float* x = src + g * src_gstride + static_cast<long long>(warp) * src_ld;
+  float4 v[kChunks];
+#pragma unroll
+  for (int k = 0; k < kChunks; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    v[k] = c < D ? *reinterpret_cast<const float4*>(x + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const RowStats st = warp_row_stats<kChunks>(v, lane, D, d_true);
+  store_centered<kChunks>(out + g * out_gstride + static_cast<long long>(warp) * out_ld, v, st.mean, lane, D, d_true);
+  if (lane == 0) rstd[g * rs_gstride + warp] = st.rstd;
+}
+
+// Expert head combine: score = sigmoid(sum_p partial[row][p][t] + b2[t]) over the
+// row-dot partials of the expert GEMM, summed in fixed order; compact output.
+__global__ void expert_combine(const float* __restrict__ partial, int n_parts, int tasks,
+                               const float* __restrict__ b2, int c_bkt, const int* __restrict__ cand_len,
+                               const int* __restrict__ out_offset, float* __restrict__ out, int rows) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const int r = row / c_bkt, c = row % c_bkt;
+  if (c >= cand_len[r]) return;
+  const float* p = partial + static_cast<long long>(row) * n_parts * tasks;
+  float* dst = out + static_cast<long long>(out_offset[r] + c) * tasks;
+  for (int t = 0; t < tasks; ++t) {
+    float acc = 0.f;
+    for (int k = 0; k < n_parts; ++k) acc += p[k * tasks + t];
+    dst[t] = sigmoid_f(acc + b2[t]);
+  }
+}
+
+}  // namespace flame
+
+namespace flame {
+
 // Embedding rows given by the caller ([R][H_bkt][d] history, [R][C_bkt][d]
-// candidates, fp32, width d) -> padded fp32 row space: history goes to the
-// block-major layout Eh[g][r*hb_bkt + i] = hist[r][g*hb_r + i] (the contiguous
-// Climber split of the ACTUAL length H_r, forward.py:50-62), candidates to
-// Ec[r*c_bkt + c].  Padding rows / columns are written as zeros.
+// candidates, fp32, width d) -> the padded row space: history goes to the
+// block-major layout row (g, r*hb_bkt + i) = hist[r][g*hb_r + i] (the contiguous
+// Climber split of the ACTUAL length H_r, forward.py:50-62), candidates to row
+// r*c_bkt + c.  Each row is written as fp32 (optional: residual input) and as
+// mean-centered bf16 + rstd (folded LN1 input).  Padding rows / cols are zero.
+struct AssembleOut {
+  float* Eh;                 // [G][R*hb_bkt][D] fp32 or null
+  float* Ec;                 // [R*c_bkt][D] fp32 or null
+  __nv_bfloat16* Ehc;        // [G][R*hb_bkt][D] centered bf16 or null
+  __nv_bfloat16* Ecc;        // [R*c_bkt][D]
+  float* rs_h;               // [G][R*hb_bkt]
+  float* rs_c;               // [R*c_bkt]
+};
+
+__device__ __forceinline__ void assemble_row(const AssembleOut& o, bool hist, long long row, const float4 (&v)[8],
+                                             int lane, int D, int d_true, bool valid) {
+  float* f = hist ? o.Eh : o.Ec;
+  if (f != nullptr) {
+    float* dst = f + row * D;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = (k * 32 + lane) * 4;
+      if (c < D) *reinterpret_cast<float4*>(dst + c) = v[k];
+    }
+  }
+  __nv_bfloat16* y = hist ? o.Ehc : o.Ecc;
+  if (y != nullptr) {
+    const RowStats st = valid ? warp_row_stats<8>(v, lane, D, d_true) : RowStats{0.f, 0.f};
+    store_centered<8>(y + row * D, v, st.mean, lane, D, d_true);
+    if (lane == 0) (hist ? o.rs_h : o.rs_c)[row] = st.rstd;
+  }
+}
+
 __global__ void scatter_embeddings(const float* __restrict__ hist, const float* __restrict__ cand,
                                    int d, int D, int R, int H_bkt, int C_bkt, int G, int hb_bkt,
                                    const int* __restrict__ hist_len, const int* __restrict__ cand_len,
-                                   float* __restrict__ Eh, float* __restrict__ Ec) {
+                                   AssembleOut o) {
   // one warp per destination row; rows [0, G*R*hb_bkt) history, then R*C_bkt candidates
   const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
@@ -172,21 +297,30 @@ __global__ void scatter_embeddings(const float* __restrict__ hist, const float* 
   const long long n_cand = static_cast<long long>(R) * C_bkt;
   if (warp >= n_hist + n_cand) return;
   const float* src = nullptr;
-  float* dst;
-  if (warp < n_hist) {
+  const bool is_hist = warp < n_hist;
+  long long row;
+  if (is_hist) {
     const int g = static_cast<int>(warp / (static_cast<long long>(R) * hb_bkt));
     const int rem = static_cast<int>(warp % (static_cast<long long>(R) * hb_bkt));
     const int r = rem / hb_bkt, i = rem % hb_bkt;
     const int hb = hist_len[r] / G;
     if (i < hb) src = hist + (static_cast<long long>(r) * H_bkt + g * hb + i) * d;
-    dst = Eh + warp * D;
+    row = warp;
   } else {
-    const long long row = warp - n_hist;
+    row = warp - n_hist;
     const int r = static_cast<int>(row / C_bkt), c = static_cast<int>(row % C_bkt);
     if (c < cand_len[r]) src = cand + row * d;
-    dst = Ec + row * D;
   }
-  for (int k = lane; k < D; k += 32) dst[k] = (src != nullptr && k < d) ? src[k] : 0.f;
+  float4 v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = (k * 32 + lane) * 4;
+    float e[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) e[q] = (src != nullptr && c + q < d) ? src[c + q] : 0.f;
+    v[k] = make_float4(e[0], e[1], e[2], e[3]);
+  }
+  assemble_row(o, is_hist, row, v, lane, D, d, src != nullptr);
 }
 
 }  // namespace flame
