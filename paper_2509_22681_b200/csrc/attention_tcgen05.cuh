@@ -47,17 +47,20 @@ struct AttnArgs {
   const int* hist_len;       // [R] actual history length H_r
   const int* cand_len;       // [R] actual candidate count C_r
   const float* scale_log2;   // [G] log2(e) / (tau_g * sqrt(head_dim))
+  int store_tma;             // 1: 128-row output tiles never cross a request (bkt % 128 == 0)
 };
 
 // Debug-only event trace of CTA 0 (set through flame_debug_attn_trace): slot 0/1 =
 // warpgroup rows 0, slot 2/3 = their control threads; entry = clock64 << 8 | code.
 __device__ unsigned long long* g_attn_trace = nullptr;
 __device__ unsigned int g_attn_trace_n[4];
+// Each slot has exactly one writer thread, which keeps its own counter
+// (trace_k, declared in each role) — no atomics on the traced path.
 #define ATTN_TRACE(slot, code)                                                            \
   do {                                                                                    \
     if (g_attn_trace != nullptr && blockIdx.x == 0 && ((slot) >= 2 ? (threadIdx.x & 31) == 0 : (threadIdx.x & 127) == 0)) { \
-      const unsigned int k_ = atomicAdd(&g_attn_trace_n[slot], 1u);                        \
-      if (k_ < 4096) g_attn_trace[(slot) * 4096 + k_] = (clock64() << 8) | (code);         \
+      if (trace_k < 4096) g_attn_trace[(slot) * 4096 + trace_k] = (clock64() << 8) | (code);  \
+      ++trace_k;                                                                          \
     }                                                                                     \
   } while (0)
 
@@ -76,13 +79,13 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 template <bool kHist>
 __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
-    const __grid_constant__ CUtensorMap tm_qkv, AttnArgs a) {
+    const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_out, AttnArgs a) {
   using namespace attn;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kWGBytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
 
   const int warp = threadIdx.x / 32;
   const int G = a.num_blocks;
@@ -90,16 +93,19 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
   const int bkt = kHist ? a.hb_bkt : a.c_bkt;
   const int n_tiles = (bkt + kRows - 1) / kRows;
 
-  // barriers of warpgroup i (12 slots each):
+  // barriers of warpgroup i (13 slots each):
   // 0 q_full (tx)  1 qs_free (128 WG + 1 control)  2,3 k_full  4,5 v_full
   // 6,7 kv_free (commit)  8 s_full (commit)  9 p_full (128)  10 o_full (commit)
-  auto B = [&](int i, int k) { return bars + i * 12 + k; };
+  // 11 vself_full (tx: the candidates' own V rows for the job's end; for history
+  //    rows a plain arrive that frees the output staging)  12 staging_ready (128)
+  auto B = [&](int i, int k) { return bars + i * 13 + k; };
   if (threadIdx.x == 256) {
     ptx::tma_prefetch_desc(&tm_qkv);
     for (int i = 0; i < 2; ++i) {
-      for (int k = 0; k < 11; ++k) ptx::mbar_init(B(i, k), 1);
+      for (int k = 0; k < 13; ++k) ptx::mbar_init(B(i, k), 1);
       ptx::mbar_init(B(i, 1), 129);
       ptx::mbar_init(B(i, 9), 128);
+      ptx::mbar_init(B(i, 12), 128);
     }
     ptx::fence_barrier_init();
   }
@@ -109,19 +115,20 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // job q (per CTA) -> unit u = blockIdx.x + (q / n_tiles) * gridDim.x, tile t = q % n_tiles;
-  // warpgroup i takes jobs q = i, i + 2, ...
+  // warpgroup i owns whole units: its k-th job is tile k % n_tiles of the CTA's
+  // unit number i + 2 * (k / n_tiles), i.e. u = blockIdx.x + that * gridDim.x; a
+  // unit's K/V is therefore loaded once per warpgroup and reused by all its tiles
   struct Job {
     bool valid;
     int u, r, g, h, t, hb, nk_all, nk, q_valid;
     int hist_row0, q_row0;
   };
-  auto job_at = [&](int q) {
+  auto job_at = [&](int wg, int jk) {
     Job j{};
-    j.u = blockIdx.x + (q / n_tiles) * gridDim.x;
+    j.u = blockIdx.x + (wg + 2 * (jk / n_tiles)) * gridDim.x;
     j.valid = j.u < n_units;
     if (!j.valid) return j;
-    j.t = q % n_tiles;
+    j.t = jk % n_tiles;
     j.h = j.u % a.nh;
     j.g = (j.u / a.nh) % G;
     j.r = j.u / (a.nh * G);
@@ -140,6 +147,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     // stays warp-uniform; one elected lane issues TMA / MMA / commits.
     const int i = warp - 8;
     const bool leader = ptx::elect_one();
+    unsigned trace_k = 0;
     uint8_t* base = smem + i * kWGBytes;
     uint8_t *sQ = base, *sKs = base + kTile, *sVs = base + 2 * kTile;
     uint8_t *sK = base + 3 * kTile, *sV = base + 5 * kTile;
@@ -147,16 +155,15 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     constexpr uint32_t idesc_s = ptx::make_idesc_bf16(kRows, kKeys, 0, 0);
     constexpr uint32_t idesc_o = ptx::make_idesc_bf16(kRows, DH, 0, 1);
     uint32_t kv_loads[2] = {0, 0}, kv_frees[2] = {0, 0};
-    int res_unit = -1;  // unit whose K/V is resident in the slots (hb <= 256)
+    int res_unit = -1;    // unit whose K/V is resident in the slots (hb <= 256)
+    int res_loaded = 0;   // chunks of res_unit already loaded
     auto load_qs = [&](const Job& j) {
       if (leader) {
-        ptx::mbar_arrive_expect_tx(B(i, 0), (kHist ? 1 : 3) * kTile);
+        // Q and the candidates' own K (s_self); their own V arrives separately
+        ptx::mbar_arrive_expect_tx(B(i, 0), (kHist ? 1 : 2) * kTile);
         const int h = j.h;
         ptx::tma_load_3d(sQ, &tm_qkv, B(i, 0), h * DH, j.q_row0, j.g);
-        if (!kHist) {
-          ptx::tma_load_3d(sKs, &tm_qkv, B(i, 0), a.DA + h * DH, j.q_row0, j.g);
-          ptx::tma_load_3d(sVs, &tm_qkv, B(i, 0), 2 * a.DA + h * DH, j.q_row0, j.g);
-        }
+        if (!kHist) ptx::tma_load_3d(sKs, &tm_qkv, B(i, 0), a.DA + h * DH, j.q_row0, j.g);
       }
       __syncwarp();
     };
@@ -178,50 +185,79 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     // K/V needed at the start of a job
     auto prepare_kv = [&](const Job& j) {
       if (j.nk_all <= 2) {
-        if (res_unit != j.u)
-          for (int c = 0; c < j.nk_all; ++c) load_kv(j, c, c);
+        if (res_unit != j.u) res_loaded = 0;
+        for (int c = res_loaded; c < j.nk_all; ++c) load_kv(j, c, c);
         res_unit = j.u;
+        res_loaded = j.nk_all;
       } else {
         res_unit = -1;
         for (int c = 0; c < 2 && c < j.nk; ++c) load_kv(j, c, c);
       }
     };
-    Job cur = job_at(i);
+    Job cur = job_at(i, 0);
     if (cur.valid) {
       load_qs(cur);
       prepare_kv(cur);
     }
+    auto load_vself = [&](const Job& jb) {  // the candidates' own V rows (needed at job end)
+      if (leader) {
+        if (kHist) {
+          ptx::mbar_arrive(B(i, 11));  // history rows: just "staging free"
+        } else {
+          ptx::mbar_arrive_expect_tx(B(i, 11), kTile);
+          ptx::tma_load_3d(sVs, &tm_qkv, B(i, 11), 2 * a.DA + jb.h * DH, jb.q_row0, jb.g);
+        }
+      }
+      __syncwarp();
+    };
+    auto issue_s = [&](const Job& jb, int c) {  // S = Q K_c^T into the WG's S columns
+      const int slot = jb.nk_all <= 2 ? c : (c & 1);
+      ptx::mbar_wait(B(i, 2 + slot), (kv_loads[slot] - 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK + slot * kTile);
+      if (leader) {
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          ptx::mma_bf16_ss(tS, ptx::make_desc_sw128(aQ + kk * 32, 16, 1024),
+                           ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
+        ptx::mma_commit(B(i, 8));
+        if (c == jb.nk - 1) ptx::mma_commit(B(i, 1));  // last read of Q for this job
+      }
+      __syncwarp();
+      ATTN_TRACE(2 + i, 13);
+    };
+    if (cur.valid) load_vself(cur);
     uint32_t n = 0, cc = 0;  // jobs / chunks processed by this warpgroup
-    for (int q = i; cur.valid; q += 2, ++n) {
-      const Job nxt = job_at(q + 2);
+    bool s0_done = false;     // S_0 of `cur` was issued at the end of the previous job
+    for (int jk = 0; cur.valid; ++jk, ++n) {
+      const Job nxt = job_at(i, jk + 1);
       ATTN_TRACE(2 + i, 11);
       const bool resident = cur.nk_all <= 2;
-      ptx::mbar_wait(B(i, 0), n & 1);  // Q (+ self tiles) landed
-      ATTN_TRACE(2 + i, 12);
-      const uint32_t aQ = ptx::smem_u32(sQ);
-      auto issue_s = [&](int c) {  // S = Q K_c^T into the WG's S columns
-        const int slot = resident ? c : (c & 1);
-        ptx::mbar_wait(B(i, 2 + slot), (kv_loads[slot] - 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t aK = ptx::smem_u32(sK + slot * kTile);
-        if (leader) {
-#pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk)
-            ptx::mma_bf16_ss(tS, ptx::make_desc_sw128(aQ + kk * 32, 16, 1024),
-                             ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
-          ptx::mma_commit(B(i, 8));
-          if (c == cur.nk - 1) ptx::mma_commit(B(i, 1));  // last read of Q this job
-        }
-        __syncwarp();
-        ATTN_TRACE(2 + i, 13);
+      // Q / K_self of `nxt` may load once the last S of `cur` completed and the WG
+      // read its q / k_self rows (qs_free phase n)
+      auto prefetch_next_q = [&]() {
+        if (!nxt.valid) return;
+        ptx::mbar_wait(B(i, 1), n & 1);
+        load_qs(nxt);
       };
-      if (cur.nk > 0) issue_s(0);
+      if (!s0_done && cur.nk > 0) {
+        ptx::mbar_wait(B(i, 0), n & 1);  // Q (+ K_self) landed
+        ATTN_TRACE(2 + i, 12);
+        issue_s(cur, 0);
+        if (cur.nk == 1) prefetch_next_q();
+      } else if (s0_done && cur.nk == 1) {
+        prefetch_next_q();
+      }
+      s0_done = false;
       for (int c = 0; c < cur.nk; ++c, ++cc) {
         const int slot = resident ? c : (c & 1);
         ptx::mbar_wait(B(i, 9), cc & 1);  // WG consumed S_c, stored P_c (and rescaled O)
         ATTN_TRACE(2 + i, 14);
         // S_{c+1} first: the warpgroup needs it next; PV_c is only needed at job end
-        if (c + 1 < cur.nk) issue_s(c + 1);
+        if (c + 1 < cur.nk) {
+          issue_s(cur, c + 1);
+          if (c + 1 == cur.nk - 1) prefetch_next_q();
+        }
         ptx::mbar_wait(B(i, 4 + slot), (kv_loads[slot] - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t aV = ptx::smem_u32(sV + slot * kTile);
@@ -229,7 +265,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
 #pragma unroll
           for (int kk = 0; kk < kKeys / 16; ++kk)
             ptx::mma_bf16_ts(tO, tP + kk * 8, ptx::make_desc_sw128(aV + kk * 16 * 128, kRows * 128, 1024),
-                             idesc_o, 1u);  // O was seeded by the warpgroup
+                             idesc_o, (c | kk) != 0);
           ptx::mma_commit(B(i, 10));
         }
         __syncwarp();
@@ -238,57 +274,83 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           if (leader) ptx::mma_commit(B(i, 6 + slot));
           __syncwarp();
           if (c + 2 < cur.nk) load_kv(cur, c + 2, slot);
-        } else if (c == cur.nk - 1 && !(nxt.valid && nxt.u == cur.u)) {
-          // unit done: every resident chunk's TMA must have landed (a causal tile
-          // may not have used all of them) before its slot can be recycled
-          for (int s = 0; s < cur.nk_all; ++s) {
-            ptx::mbar_wait(B(i, 2 + s), (kv_loads[s] - 1) & 1);
-            ptx::mbar_wait(B(i, 4 + s), (kv_loads[s] - 1) & 1);
-            if (leader) ptx::mma_commit(B(i, 6 + s));
-            __syncwarp();
+        } else if (!(nxt.valid && nxt.u == cur.u)) {
+          // last job of this unit: recycle slot c as soon as PV_c is issued and,
+          // when the next unit is resident too, start loading its chunk c into it
+          if (leader) ptx::mma_commit(B(i, 6 + slot));
+          __syncwarp();
+          if (nxt.valid && nxt.nk_all <= 2 && c < nxt.nk_all) {
+            if (res_unit != nxt.u) { res_unit = nxt.u; res_loaded = 0; }
+            load_kv(nxt, c, c);
+            res_loaded = c + 1;
+          }
+          if (c == cur.nk - 1) {
+            // chunks this (causal) tile never used: their TMA must land before reuse
+            for (int s = cur.nk; s < cur.nk_all; ++s) {
+              ptx::mbar_wait(B(i, 2 + s), (kv_loads[s] - 1) & 1);
+              ptx::mbar_wait(B(i, 4 + s), (kv_loads[s] - 1) & 1);
+              if (leader) ptx::mma_commit(B(i, 6 + s));
+              __syncwarp();
+            }
           }
         }
-      }
-      // Q / self tiles are free once the last S completed and the WG read its rows
-      if (cur.nk > 0 && nxt.valid) {
-        ptx::mbar_wait(B(i, 1), n & 1);
-        load_qs(nxt);
       }
       if (cur.nk == 0) {
         if (leader) ptx::mbar_arrive(B(i, 1));
         __syncwarp();
-        if (nxt.valid) {
-          ptx::mbar_wait(B(i, 1), n & 1);
-          load_qs(nxt);
+        prefetch_next_q();
+      }
+      if (nxt.valid) {
+        prepare_kv(nxt);
+        // head start: the next job's first S runs while this job's output drains
+        if (nxt.nk > 0) {
+          ptx::mbar_wait(B(i, 0), (n + 1) & 1);
+          issue_s(nxt, 0);
+          s0_done = true;
         }
       }
-      if (nxt.valid) prepare_kv(nxt);
+      // this job's output: the WG staged its rows (or wrote them directly); store the
+      // tile, then reuse the staging buffer for the next job's V_self
+      ptx::mbar_wait(B(i, 12), n & 1);
+      if (a.store_tma) {
+        if (leader) {
+          ptx::tma_store_3d(&tm_out, sVs, cur.h * DH, cur.q_row0, cur.g);
+          ptx::tma_store_commit();
+          ptx::tma_store_wait_read<0>();
+        }
+        __syncwarp();
+      }
+      if (nxt.valid) load_vself(nxt);
       cur = nxt;
     }
+    if (leader) ptx::tma_store_wait<0>();
+    __syncwarp();
   } else if (warp < 8) {
     // ------------------------------------------------- softmax / epilogue rows
     const int i = warp >> 2;
     const int row = threadIdx.x & 127;  // query row within the tile == TMEM lane
+    unsigned trace_k = 0;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + i * 256 + lane_base, tP = tS + 128, tO = tS + 192;
     const uint8_t* base = smem + i * kWGBytes;
     const uint8_t *sQ = base, *sKs = base + kTile, *sVs = base + 2 * kTile;
+    uint8_t* stage = smem + i * kWGBytes + 2 * kTile;  // = the V_self tile; reused as output staging
     uint32_t n = 0, cc = 0;
-    Job nj = job_at(i);
-    for (int q = i;; q += 2, ++n) {
+    Job nj = job_at(i, 0);
+    for (int jk = 0;; ++jk, ++n) {
       const Job j = nj;
       ATTN_TRACE(i, 1);
       if (!j.valid) break;
-      nj = job_at(q + 2);  // metadata loads overlap this job
+      nj = job_at(i, jk + 1);  // metadata loads overlap this job
       const int qi = j.t * kRows + row;
       const bool row_ok = qi < j.q_valid;
       const float sl2 = a.scale_log2[j.g];
       float m_self, m, l;
-      uint32_t seed[DH];
       ptx::mbar_wait(B(i, 0), n & 1);
       ATTN_TRACE(i, 2);
-      // seed the TMEM accumulator O with v_self (weight exp2(s_self - m) = 1 at
-      // m = s_self); history rows start from O = 0, m = -inf, l = 0
+      // the diagonal of the SUMI mask: s_self = q . k_self (attention.py:134) seeds
+      // m = s_self, l = 1; its value term is added at the end.  History rows start
+      // empty (m = -inf, l = 0).
       if (!kHist) {
         float dot = 0.f;
 #pragma unroll
@@ -296,35 +358,25 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           const uint32_t off = ptx::sw128_offset(row, c * 16);
           const uint4 qv = *reinterpret_cast<const uint4*>(sQ + off);
           const uint4 kv = *reinterpret_cast<const uint4*>(sKs + off);
-          const uint4 vv = *reinterpret_cast<const uint4*>(sVs + off);
           const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(&qv);
           const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
-          const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vv);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 qf = __bfloat1622float2(q2[e]);
             const float2 kf = __bfloat1622float2(k2[e]);
             dot = fmaf(qf.x, kf.x, dot);
             dot = fmaf(qf.y, kf.y, dot);
-            const float2 v = __bfloat1622float2(v2[e]);
-            seed[c * 8 + 2 * e] = __float_as_uint(v.x);
-            seed[c * 8 + 2 * e + 1] = __float_as_uint(v.y);
           }
         }
         m_self = dot * sl2;
         m = m_self;
         l = 1.f;
       } else {
-#pragma unroll
-        for (int e = 0; e < DH; ++e) seed[e] = 0u;
         m_self = -INFINITY;
         m = -INFINITY;
         l = 0.f;
       }
-#pragma unroll
-      for (int k = 0; k < DH / 16; ++k)
-        ptx::tmem_st_32x32b_x16(tO + k * 16, *reinterpret_cast<uint32_t(*)[16]>(seed + k * 16));
-      ptx::mbar_arrive(B(i, 1));  // q / self rows read
+      ptx::mbar_arrive(B(i, 1));  // q / k_self rows read
       for (int c = 0; c < j.nk; ++c, ++cc) {
         const int key0 = c * kKeys;
         int key_lim = j.hb - key0;  // keys with local index < key_lim are valid
@@ -344,9 +396,15 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           for (int e = 0; e < kKeys; ++e)
             if (e >= key_lim) s[e] = __float_as_uint(-INFINITY);
         }
-        float cmax = -INFINITY;
+        // tree reductions (8 independent chains): only two warps share a scheduler,
+        // so a serial max / sum chain would be latency-bound
+        float mx[8];
 #pragma unroll
-        for (int e = 0; e < kKeys; ++e) cmax = fmaxf(cmax, __uint_as_float(s[e]));
+        for (int q = 0; q < 8; ++q) mx[q] = __uint_as_float(s[q]);
+#pragma unroll
+        for (int e = 8; e < kKeys; ++e) mx[e & 7] = fmaxf(mx[e & 7], __uint_as_float(s[e]));
+        const float cmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         // raise the reference max only when the chunk max exceeds it by > 2^8
         const float cm = cmax * sl2;
         const bool raise = (m == -INFINITY) ? (cm != -INFINITY) : (cm - m > kRescaleThreshold);
@@ -355,31 +413,47 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
         m = m_new;
         const float m_use = (m == -INFINITY) ? 0.f : m;
         // p = exp2(s*scale - m), packed to bf16 pairs in place (s[e/2] is dead)
-        float psum = 0.f;
+        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (full) {
+          // one pair in four on the FMA pipe (polynomial exp2): the MUFU is the
+          // softmax bottleneck with two warpgroups per SM
 #pragma unroll
-        for (int e = 0; e < kKeys; e += 2) {
-          const float p0 = ptx::exp2_approx(fmaf(__uint_as_float(s[e]), sl2, -m_use));
-          const float p1 = ptx::exp2_approx(fmaf(__uint_as_float(s[e + 1]), sl2, -m_use));
-          psum += p0 + p1;
-          s[e / 2] = pack_bf16x2(p0, p1);
+          for (int e = 0; e < kKeys; e += 2) {
+            const float x0 = fmaf(__uint_as_float(s[e]), sl2, -m_use);
+            const float x1 = fmaf(__uint_as_float(s[e + 1]), sl2, -m_use);
+            const bool poly = ((e >> 1) & 3) == 3;
+            const float p0 = poly ? ptx::exp2_poly3(x0) : ptx::exp2_approx(x0);
+            const float p1 = poly ? ptx::exp2_poly3(x1) : ptx::exp2_approx(x1);
+            ps[(e >> 1) & 7] += p0 + p1;
+            s[e / 2] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < kKeys; e += 2) {
+            const float p0 = ptx::exp2_approx(fmaf(__uint_as_float(s[e]), sl2, -m_use));
+            const float p1 = ptx::exp2_approx(fmaf(__uint_as_float(s[e + 1]), sl2, -m_use));
+            ps[(e >> 1) & 7] += p0 + p1;
+            s[e / 2] = pack_bf16x2(p0, p1);
+          }
         }
+        const float psum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
         l = l * alpha + psum;
-        // PV(c-1) must be done before P is overwritten and O rescaled
         if (c > 0) {
+          // PV(c-1) must be done before P is overwritten and O rescaled
           ptx::mbar_wait(B(i, 10), (cc - 1) & 1);
           ptx::tc_fence_after();
-        }
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
-          uint32_t ov[DH];
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            uint32_t ov[DH];
 #pragma unroll
-          for (int k = 0; k < DH / 32; ++k)
-            ptx::tmem_ld_32x32b_x32(tO + k * 32, *reinterpret_cast<uint32_t(*)[32]>(ov + k * 32));
-          ptx::tmem_ld_wait();
+            for (int k = 0; k < DH / 32; ++k)
+              ptx::tmem_ld_32x32b_x32(tO + k * 32, *reinterpret_cast<uint32_t(*)[32]>(ov + k * 32));
+            ptx::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < DH; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            for (int e = 0; e < DH; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
 #pragma unroll
-          for (int k = 0; k < DH / 16; ++k)
-            ptx::tmem_st_32x32b_x16(tO + k * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + k * 16));
+            for (int k = 0; k < DH / 16; ++k)
+              ptx::tmem_st_32x32b_x16(tO + k * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + k * 16));
+          }
         }
 #pragma unroll
         for (int k = 0; k < kKeys / 32; ++k)
@@ -389,15 +463,11 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
         ptx::mbar_arrive(B(i, 9));
         ATTN_TRACE(i, 4);
       }
-      // out = O / l  (O already holds exp2(s_self - m) v_self)
+      // out = (O + exp2(s_self - m) v_self) / l
       float o[DH];
       if (j.nk > 0) {
         ptx::mbar_wait(B(i, 10), (cc - 1) & 1);
         ptx::tc_fence_after();
-      } else {
-        ptx::tmem_st_wait();
-      }
-      {
         uint32_t ov[DH];
 #pragma unroll
         for (int k = 0; k < DH / 32; ++k)
@@ -406,10 +476,41 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
 #pragma unroll
         for (int e = 0; e < DH; ++e) o[e] = __uint_as_float(ov[e]);
         ptx::tc_fence_before();
+      } else {
+#pragma unroll
+        for (int e = 0; e < DH; ++e) o[e] = 0.f;
       }
       ATTN_TRACE(i, 5);
-      if (row_ok) {
-        const float inv = 1.f / l;
+      ptx::mbar_wait(B(i, 11), n & 1);  // V_self rows of this job (history: staging free)
+      if (!kHist) {
+        const float w_self = ptx::exp2_approx(m_self - (m == -INFINITY ? 0.f : m));
+#pragma unroll
+        for (int c = 0; c < DH / 8; ++c) {
+          const uint4 vv = *reinterpret_cast<const uint4*>(stage + ptx::sw128_offset(row, c * 16));
+          const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vv);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 v = __bfloat1622float2(v2[e]);
+            o[c * 8 + 2 * e] = fmaf(w_self, v.x, o[c * 8 + 2 * e]);
+            o[c * 8 + 2 * e + 1] = fmaf(w_self, v.y, o[c * 8 + 2 * e + 1]);
+          }
+        }
+      }
+      const float inv = 1.f / l;
+      if (a.store_tma) {
+        // stage the bf16 rows over the V_self tile (each thread rewrites exactly the
+        // row it just read); the control warp TMA-stores the 128 x 64 tile
+#pragma unroll
+        for (int c = 0; c < DH / 8; ++c) {
+          uint4 w;
+          w.x = pack_bf16x2(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
+          w.y = pack_bf16x2(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
+          w.z = pack_bf16x2(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
+          w.w = pack_bf16x2(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
+          *reinterpret_cast<uint4*>(stage + ptx::sw128_offset(row, c * 16)) = w;
+        }
+        ptx::fence_proxy_async_smem();
+      } else if (row_ok) {
         __nv_bfloat16* dst = a.out + j.g * a.out_gstride + static_cast<long long>(j.q_row0 + row) * a.out_ld + j.h * DH;
 #pragma unroll
         for (int c = 0; c < DH / 8; ++c) {
@@ -421,7 +522,9 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           reinterpret_cast<uint4*>(dst)[c] = w;
         }
       }
+      ptx::mbar_arrive(B(i, 12));  // staging written / V_self rows consumed
     }
+
   }
   ptx::tc_fence_before();
   __syncthreads();

@@ -538,10 +538,15 @@ struct Pipe {
       a.nh = c->nh;
       const int units = e->R * c->G * c->nh;  // persistent: one CTA per SM walks the units
       dim3 tgrid(units < c->num_sms ? units : c->num_sms);
+      CUtensorMap tm_out;  // attention output tiles (128 rows x 64 cols of one head) via TMA
+      if (!make_tmap_bf16_3d(&tm_out, e->AO, c->DA, e->rows, c->G, static_cast<uint64_t>(c->DA) * 2,
+                             e->rows * static_cast<uint64_t>(c->DA) * 2, 64, 128))
+        return fail(2, "tensor map for attention output failed");
+      a.store_tma = ((hist ? e->hb_bkt : e->c_bkt) % 128) == 0;
       if (hist)
-        sumi_attention_tcgen05<true><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
+        sumi_attention_tcgen05<true><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, tm_out, a);
       else
-        sumi_attention_tcgen05<false><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, a);
+        sumi_attention_tcgen05<false><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, tm_out, a);
     } else {
       AttnArgsF32 a{};
       a.qkv = act(e->QKV); a.out = act(e->AO);
