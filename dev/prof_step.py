@@ -21,5 +21,22 @@ for _ in range(passes):
     ex.run(_lib.INPUT_IDS, graph=False)
 ex.stream.synchronize()
 print("launches per pass", ex.launch_count())
-for rec in ex.profile(_lib.INPUT_IDS):
-    print(f"{rec['name']:>18s} {rec['ms']:8.3f} ms  {rec['flops']/max(rec['ms'],1e-9)/1e9:8.1f} TF/s  {rec['bytes']/max(rec['ms'],1e-9)/1e6:8.1f} GB/s")
+import statistics
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    hnd = pynvml.nvmlDeviceGetHandleByIndex(0)
+except Exception:
+    hnd = None
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 7
+runs, clocks = [], []
+for _ in range(reps):
+    runs.append(ex.profile(_lib.INPUT_IDS))
+    if hnd is not None:
+        clocks.append(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM))
+tot = 0.0
+for i, rec in enumerate(runs[0]):
+    ms = statistics.median(r[i]["ms"] for r in runs)
+    tot += ms
+    print(f"{rec['name']:>18s} {ms:8.3f} ms  {rec['flops']/max(ms,1e-9)/1e9:8.1f} TF/s  {rec['bytes']/max(ms,1e-9)/1e6:8.1f} GB/s")
+print(f"{'sum':>18s} {tot:8.3f} ms   sm clocks {clocks}")

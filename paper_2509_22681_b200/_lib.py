@@ -8,10 +8,12 @@ or PyTorch implementation.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_flame_b200.so"
+# FLAME_B200_LIB: load an alternative build of the same library (dev A/B variants)
+LIB_PATH = Path(os.environ.get("FLAME_B200_LIB") or Path(__file__).resolve().parent / "_flame_b200.so")
 
 FLAME_BF16, FLAME_FP32 = 0, 1
 INPUT_EMBEDDINGS, INPUT_IDS, INPUT_GATHER_ONLY = 0, 1, 2

@@ -147,3 +147,45 @@ __device__ __forceinline__ void stage_row32(uint8_t* box, int r, const float (&v
 }
 
 }  // namespace flame
+
+// ------------------------------------------------------------ fp32 pairs
+// fma.rn.f32x2 (FFMA2) does two fp32 FMAs per lane per instruction at the
+// issue rate of one scalar FFMA.  A pair lives in a 64-bit register pair.
+namespace f2 {
+__device__ __forceinline__ uint64_t make(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void split(uint64_t r, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// tanh-form GELU on a pair: hx (1 + tanh(x (k0 + k1 x^2))), hx = x / 2
+__device__ __forceinline__ uint64_t gelu(uint64_t x) {
+  const uint64_t k0 = make(0.7978845608028654f, 0.7978845608028654f);
+  const uint64_t k1 = make(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
+  const uint64_t h = make(0.5f, 0.5f);
+  const uint64_t z = mul(x, fma(mul(x, x), k1, k0));
+  float z0, z1;
+  split(z, z0, z1);
+  asm("tanh.approx.f32 %0, %0;" : "+f"(z0));
+  asm("tanh.approx.f32 %0, %0;" : "+f"(z1));
+  const uint64_t hx = mul(x, h);
+  return fma(hx, make(z0, z1), hx);
+}
+}  // namespace f2

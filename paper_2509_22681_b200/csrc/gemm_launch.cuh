@@ -2,6 +2,7 @@
 // fused epilogue) — shared by the model pipeline and the debug entry points.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include "gemm_tcgen05.cuh"
 #include "tmap.cuh"
 
@@ -19,21 +20,49 @@ struct GemmProblem {
   int epi;  // EPI_* flags
 };
 
+// 2-CTA clusters (W tile multicast) unless FLAME_GEMM_CLUSTER=1
+static int gemm_cluster_pref() {
+  static int v = [] {
+    const char* e = getenv("FLAME_GEMM_CLUSTER");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return v;
+}
+
 template <int BN, int EPI>
 static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_sms) {
   using C = gemm::Cfg<BN, EPI>;
   static bool attr_set = false;
+  static int max_clusters = 0;  // co-resident 2-CTA clusters at this smem size
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, EPI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t q = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    q.gridDim = dim3(2 * ((num_sms + 1) / 2));
+    q.blockDim = dim3(C::kThreads);
+    q.dynamicSmemBytes = C::kSmemBytes;
+    q.attrs = at;
+    q.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, gemm_bf16_tcgen05<BN, EPI>, &q) != cudaSuccess) {
+      cudaGetLastError();
+      max_clusters = 0;
+    }
     attr_set = true;
   }
+  const int m_tiles = (p.M + gemm::BM - 1) / gemm::BM;
+  const int n_tiles = (p.N + BN - 1) / BN;
+  const int ncl = (gemm_cluster_pref() == 2 && m_tiles >= 2 && max_clusters > 0) ? 2 : 1;
   CUtensorMap ta, tb;
   const int ga = p.a_shared ? 1 : p.G;
   if (!make_tmap_bf16_3d(&ta, p.A, p.K, p.M, ga, p.lda * 2, p.a_gstride * 2, gemm::BK, gemm::BM))
     return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_3d(&tb, p.W, p.K, p.N, p.G, p.ldw * 2, p.w_gstride * 2, gemm::BK, BN))
+  if (!make_tmap_bf16_3d(&tb, p.W, p.K, p.N, p.G, p.ldw * 2, p.w_gstride * 2, gemm::BK, BN / ncl))
     return cudaErrorInvalidValue;
   CUtensorMap to;
   constexpr int ob = (EPI & EPI_OUT_F32) ? 4 : 2;
@@ -44,21 +73,42 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
                                p.ep.out_ld * ob, p.ep.out_gstride * ob)) {
     return cudaErrorInvalidValue;
   }
-  CUtensorMap to2 = to;
+  CUtensorMap to2 = to, tr = to;
+  if constexpr (C::kResidTma) {
+    if (!make_tmap_out_3d(&tr, const_cast<float*>(p.ep.resid), 4, p.N, p.M, p.ep.resid_gstride ? p.G : 1,
+                          p.ep.resid_ld * 4, p.ep.resid_gstride * 4))
+      return cudaErrorInvalidValue;
+  }
   if constexpr (C::kDual) {
     if (!make_tmap_out_3d(&to2, p.ep.out2, 2, p.N, p.M, p.G, p.ep.out2_ld * 2, p.ep.out2_gstride * 2))
       return cudaErrorInvalidValue;
   }
-  const int m_tiles = (p.M + gemm::BM - 1) / gemm::BM;
-  const int n_tiles = (p.N + BN - 1) / BN;
-  const int total = p.G * m_tiles * n_tiles;
-  const int grid = total < num_sms ? total : num_sms;
   GemmEpilogue ep = p.ep;
   ep.M = p.M;
   ep.N = p.N;
-  gemm_bf16_tcgen05<BN, EPI><<<grid, C::kThreads, C::kSmemBytes, s>>>(
-      ta, tb, to, to2, p.K / gemm::BK, m_tiles, n_tiles, p.G, p.a_shared, ep);
-  return cudaGetLastError();
+  if (ncl == 1) {
+    const int total = p.G * m_tiles * n_tiles;
+    const int grid = total < num_sms ? total : num_sms;
+    gemm_bf16_tcgen05<BN, EPI><<<grid, C::kThreads, C::kSmemBytes, s>>>(
+        ta, tb, to, to2, tr, p.K / gemm::BK, m_tiles, n_tiles, p.G, p.a_shared, ep);
+    return cudaGetLastError();
+  }
+  const int total_pairs = p.G * ((m_tiles + 1) / 2) * n_tiles;
+  const int clusters = total_pairs < max_clusters ? total_pairs : max_clusters;
+  cudaLaunchConfig_t q = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  q.gridDim = dim3(2 * clusters);
+  q.blockDim = dim3(C::kThreads);
+  q.dynamicSmemBytes = C::kSmemBytes;
+  q.stream = s;
+  q.attrs = at;
+  q.numAttrs = 1;
+  return cudaLaunchKernelEx(&q, gemm_bf16_tcgen05<BN, EPI>, ta, tb, to, to2, tr, p.K / gemm::BK, m_tiles, n_tiles,
+                            p.G, p.a_shared, ep);
 }
 
 template <int BN>
@@ -94,7 +144,7 @@ static cudaError_t launch_gemm_bn(const GemmProblem& p, cudaStream_t s, int num_
 static int gemm_row_parts(int N, int epi) {
   const int bn = N >= 256 ? 256 : 128;
   const bool heavy = (epi & (EPI_GELU | EPI_LNSTATS | EPI_STATS)) != 0;
-  return ((N + bn - 1) / bn) * (heavy ? 3 : 2);
+  return ((N + bn - 1) / bn) * (heavy ? FLAME_GEMM_HEAVY_WARPS / 4 : 2);
 }
 
 static cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t s, int num_sms) {

@@ -13,7 +13,14 @@
 //                 other 32-column chunk: tcgen05.ld -> bias / tanh-GELU / fp32
 //                 residual in registers -> swizzled smem box -> TMA bulk store
 // The epilogue of tile i overlaps the MMAs of tile i+1 through the second
-// accumulator buffer.  The K loop order is fixed per row, so a row's result is
+// accumulator buffer.
+// Launched with 2-CTA clusters along M, the two CTAs of a cluster work on
+// vertically adjacent tiles of the same column block in lock step: each loads
+// its own A tile plus HALF of the shared W tile, multicast into both CTAs'
+// smem, so the L2->SM operand traffic per CTA drops from (BM+BN) to (BM+BN/2)
+// rows per k-block (the GEMMs here are L2-bandwidth-bound at 128 x 256 tiles).
+// A stage is refilled only after both CTAs' MMAs released it (empty barriers
+// count 2 arrivals, committed by multicast).  The K loop order is fixed per row, so a row's result is
 // independent of which tile / batch position it lands in (batch invariance:
 // chunked == unchunked, duplicate candidates give identical scores).
 #pragma once
@@ -76,21 +83,45 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kSmemBudget = 227 * 1024;
 
-// Per-variant configuration: heavy epilogues (GELU, folded LayerNorm) get 12
-// epilogue warps (3 per TMEM lane quadrant) so they keep up with the MMAs; the
-// smem ring gets whatever the staging boxes leave (up to 6 stages).
+// Per-variant configuration.  The epilogue does its arithmetic on fp32 pairs
+// (fma.rn.f32x2: twice the FMA-pipe throughput of scalar FFMA) and prefetches
+// the next TMEM chunk while processing the current one, so two warps per TMEM
+// lane quadrant keep up with the MMAs (FLAME_GEMM_HEAVY_WARPS=12 restores three
+// for the GELU / LayerNorm variants).  Per-column vectors (bias, folded-LN
+// column sums u) of bf16-output variants are staged once per tile into a
+// per-warp smem slice and read back as broadcasts.  The smem ring gets whatever
+// the staging boxes leave (up to 6 stages).
+#ifndef FLAME_GEMM_HEAVY_WARPS
+#define FLAME_GEMM_HEAVY_WARPS 8
+#endif
 template <int BN, int EPI>
 struct Cfg {
   static constexpr bool kHeavy = (EPI & (EPI_GELU | EPI_LNSTATS | EPI_STATS)) != 0;
-  static constexpr int kEpiWarps = kHeavy ? 12 : 8;
+  static constexpr int kEpiWarps = kHeavy ? FLAME_GEMM_HEAVY_WARPS : 8;
+  static constexpr int kEpiPerQuad = kEpiWarps / 4;
   static constexpr int kThreads = 128 + 32 * kEpiWarps;
+  static constexpr bool kF32 = (EPI & EPI_OUT_F32) != 0;
+  static constexpr bool kRowDot = (EPI & EPI_ROWDOT) != 0;
   // STATS with an fp32 primary output also emits a bf16 copy (second TMA store)
-  static constexpr bool kDual = (EPI & EPI_STATS) != 0 && (EPI & EPI_OUT_F32) != 0;
-  static constexpr int kBoxBytes = 32 * 32 * 4 + (kDual ? 32 * 32 * 2 : 0);
+  static constexpr bool kDual = (EPI & EPI_STATS) != 0 && kF32;
+  static constexpr int kOutBoxes = 1;
+  static constexpr int kOutBoxBytes = kRowDot ? 0 : 32 * 32 * (kF32 ? 4 : 2);
+  static constexpr int kBoxBytes = kOutBoxes * kOutBoxBytes + (kDual ? 32 * 32 * 2 : 0);
+  // chunks of 32 columns per warp and the per-warp column-vector slices
+  static constexpr int kChunks = BN / 32;
+  static constexpr int kMyChunks = (kChunks + kEpiPerQuad - 1) / kEpiPerQuad;
+  static constexpr bool kBiasSmem = (EPI & EPI_BIAS) != 0 && !kF32;
+  static constexpr bool kUSmem = (EPI & EPI_LNSTATS) != 0;
+  static constexpr int kCvecs = (kBiasSmem ? 1 : 0) + (kUSmem ? 1 : 0);
+  static constexpr int kCvecBytes = kCvecs * kMyChunks * 32 * 4;
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kFixed = kEpiWarps * kBoxBytes + 1024 /*align*/ + 256 /*barriers*/;
+  // fp32 residuals are TMA-loaded as 32x32 boxes (row-per-lane global loads
+  // would cost one L1 wavefront per 16 bytes), two boxes in flight per warp
+  static constexpr bool kResidTma = (EPI & EPI_RESID) != 0 && (EPI & EPI_RESID_BF16) == 0;
+  static constexpr int kResidBytes = kResidTma ? 2 * 32 * 32 * 4 : 0;
+  static constexpr int kFixed = kEpiWarps * (kBoxBytes + kCvecBytes + kResidBytes) + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int kStagesFit = (kSmemBudget - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
   static_assert(kStages >= 2, "GEMM smem ring too shallow");
@@ -104,7 +135,7 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
-                      int num_k_blocks, int m_tiles, int n_tiles, int groups, int a_shared, GemmEpilogue ep) {
+                      const __grid_constant__ CUtensorMap tmR, int num_k_blocks, int m_tiles, int n_tiles, int groups, int a_shared, GemmEpilogue ep) {
   using C = gemm::Cfg<BN, EPI>;
   constexpr int kEpiWarps = C::kEpiWarps;
   constexpr int kEpiPerQuad = kEpiWarps / 4;
@@ -116,29 +147,42 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * C::kABytes;
   uint8_t* smem_box = smem + kStages * C::kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_box + kEpiWarps * C::kBoxBytes);
+  uint8_t* smem_cvec = smem_box + kEpiWarps * C::kBoxBytes;
+  uint8_t* smem_resid = smem_cvec + kEpiWarps * C::kCvecBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_resid + kEpiWarps * C::kResidBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tmem_full = bars + 2 * kStages;
   uint64_t* tmem_empty = bars + 2 * kStages + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* resid_full = bars + 2 * kStages + 4;  // [kEpiWarps][2]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4 + 2 * kEpiWarps);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  // cluster geometry (1 or 2 CTAs along M); a cluster walks pair-tiles
+  const int ncl = static_cast<int>(ptx::cluster_nctarank());
+  const int crank = static_cast<int>(ptx::cluster_ctarank());
+  const int m_pairs = (m_tiles + ncl - 1) / ncl;
+  const int cid = blockIdx.x / ncl;
+  const int nclusters = gridDim.x / ncl;
+  const int total_tiles = groups * m_pairs * n_tiles;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
     ptx::tma_prefetch_desc(&tmO);
     if (C::kDual) ptx::tma_prefetch_desc(&tmO2);
+    if (C::kResidTma) ptx::tma_prefetch_desc(&tmR);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], ncl);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tmem_full[s], 1);
       ptx::mbar_init(&tmem_empty[s], kEpiWarps);
     }
+    if (C::kResidTma)
+      for (int s = 0; s < 2 * kEpiWarps; ++s) ptx::mbar_init(&resid_full[s], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_base_slot);
@@ -146,8 +190,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
-
-  const int total_tiles = groups * m_tiles * n_tiles;
+  if (ncl > 1) ptx::cluster_sync();  // peer barriers initialised before any multicast
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -155,21 +198,40 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     const bool leader = ptx::elect_one();
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = cid; tile < total_tiles; tile += nclusters) {
       const int n_blk = tile % n_tiles;
-      const int m_blk = (tile / n_tiles) % m_tiles;
-      const int g = tile / (n_tiles * m_tiles);
+      // the odd tail CTA of a cluster recomputes the last tile; its stores fall past M
+      const int m_blk = min(((tile / n_tiles) % m_pairs) * ncl + crank, m_tiles - 1);
+      const int g = tile / (n_tiles * m_pairs);
       const int ga = a_shared ? 0 : g;
       for (int kb = 0; kb < num_k_blocks; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
+#ifdef FLAME_DBG_GEMM_NO_TMA
+        if (leader) ptx::mbar_arrive(&full[stage]);
+        if (false) {
+#else
         if (leader) {
+#endif
           ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
           ptx::tma_load_3d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * gemm::BK,
                            m_blk * gemm::BM, ga);
-          ptx::tma_load_3d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * gemm::BK,
-                           n_blk * BN, g);
+          if (ncl == 1) {
+            ptx::tma_load_3d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * gemm::BK,
+                             n_blk * BN, g);
+          } else {
+            ptx::tma_load_3d_mc(smem_b + stage * C::kBBytes + crank * (C::kBBytes / 2), &tmB, &full[stage],
+                                kb * gemm::BK, n_blk * BN + crank * (BN / 2), g, 0x3);
+          }
         }
         __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+    if (ncl > 1) {
+      // drain: every stage released by both CTAs' MMAs, so no multicast arrival
+      // is still in flight towards this CTA when it exits
+      for (int i = 0; i < kStages; ++i) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
@@ -181,7 +243,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = cid; tile < total_tiles; tile += nclusters) {
       ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -197,7 +259,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
             const uint64_t bd = ptx::make_desc_sw128(b_addr + k * 32, 16, 1024);
             ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          ptx::mma_commit(&empty[stage]);
+          if (ncl == 1) ptx::mma_commit(&empty[stage]);
+          else ptx::mma_commit_mc(&empty[stage], 0x3);
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -208,19 +271,75 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     }
   } else if (warp >= 4) {
     // ----------------------------------------------------------- epilogue
-    constexpr bool kF32 = (EPI & EPI_OUT_F32) != 0;
+    constexpr bool kF32 = C::kF32;
+    constexpr int kChunks = C::kChunks;
     const int ew = warp - 4;
     const int wq = warp & 3;    // TMEM lane quadrant this warp may access
     const int half = ew >> 2;   // which interleaved share of the 32-column chunks
     uint8_t* box = smem_box + ew * C::kBoxBytes;
-    uint8_t* box2 = box + 32 * 32 * 4;  // bf16 side-output box (kDual)
+    uint8_t* box2 = box + C::kOutBoxBytes;  // bf16 side-output box (kDual)
+    int box_i = 0;                           // alternating staging box (bf16 outputs)
     const bool epi_leader = ptx::elect_one();  // same lane issues stores and waits (bulk groups are per thread)
+    // fp32 residual stream: this warp's valid chunks of all its tiles, in order;
+    // position p lives in buffer p & 1 and is loaded while position p - 2 is consumed
+    uint8_t* rbuf = smem_resid + ew * C::kResidBytes;
+    uint64_t* rfull = resid_full + 2 * ew;
+    auto nk_of = [&](int t) {
+      const int nb = t % n_tiles;
+      int n = 0;
+#pragma unroll
+      for (int k = 0; k < C::kMyChunks; ++k)
+        n += (half + k * kEpiPerQuad < kChunks && nb * BN + (half + k * kEpiPerQuad) * 32 < ep.N) ? 1 : 0;
+      return n;
+    };
+    int ld_t = cid, ld_k = 0, ld_buf = 0, rd_buf = 0;
+    uint32_t rd_phase = 0;  // bit b: parity of buffer b's next completion
+    auto ld_advance = [&](bool step) {
+      if (step) ++ld_k;
+      while (ld_t < total_tiles && ld_k >= nk_of(ld_t)) {
+        ld_t += nclusters;
+        ld_k = 0;
+      }
+    };
+    auto ld_issue = [&]() {
+      if (ld_t >= total_tiles) return;
+      if (epi_leader) {
+        const int nb = ld_t % n_tiles;
+        const int mb = ((ld_t / n_tiles) % m_pairs) * ncl + crank;
+        const int gg = ld_t / (n_tiles * m_pairs);
+        const int c0 = nb * BN + (half + ld_k * kEpiPerQuad) * 32;
+        const int r0 = min(mb * gemm::BM + wq * 32, ep.M - 1);
+        ptx::mbar_arrive_expect_tx(&rfull[ld_buf], 32 * 32 * 4);
+        ptx::tma_load_3d(rbuf + ld_buf * 4096, &tmR, &rfull[ld_buf], c0, r0, ep.resid_gstride ? gg : 0);
+      }
+      ld_buf ^= 1;
+      ld_advance(true);
+    };
+    if constexpr (C::kResidTma) {
+      ld_advance(false);
+      ld_issue();
+      ld_issue();
+    }
+    float* cv_bias = reinterpret_cast<float*>(smem_cvec + ew * C::kCvecBytes);
+    float* cv_u = cv_bias + (C::kBiasSmem ? C::kMyChunks * 32 : 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = cid; tile < total_tiles; tile += nclusters) {
       const int n_blk = tile % n_tiles;
-      const int m_blk = (tile / n_tiles) % m_tiles;
-      const int g = tile / (n_tiles * m_tiles);
+      const int m_blk = ((tile / n_tiles) % m_pairs) * ncl + crank;  // may be m_tiles (tail): rows >= M
+      const int g = tile / (n_tiles * m_pairs);
+      if constexpr (C::kCvecs > 0) {
+        // this warp's slice of the per-column vectors, fetched while the MMAs run
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < C::kMyChunks; ++k) {
+          const int col = n_blk * BN + (half + k * kEpiPerQuad) * 32 + lane;
+          const bool ok = half + k * kEpiPerQuad < kChunks && col < ep.N;
+          if constexpr (C::kBiasSmem) cv_bias[k * 32 + lane] = ok ? __ldg(ep.bias + g * ep.bias_gstride + col) : 0.f;
+          if constexpr (C::kUSmem) cv_u[k * 32 + lane] = ok ? __ldg(ep.colsum + g * ep.colsum_gstride + col) : 0.f;
+        }
+        __syncwarp();
+      }
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
       ptx::tc_fence_after();
       const int row0 = m_blk * gemm::BM + wq * 32;
@@ -242,77 +361,176 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
         ln_mean = s1 / ep.d_true;
         rs = rsqrtf(fmaxf(s2 / ep.d_true - ln_mean * ln_mean, 0.f) + 1e-5f);
       }
-      float st_sum = 0.f, st_sq = 0.f;
-      float dot[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-      for (int c = half; c < BN / 32; c += kEpiPerQuad) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
-        ptx::tmem_ld_wait();
+      // LN(x) W + b = rs * acc + (b - rs * mean * u)
+      const uint64_t rs2 = f2::make(rs, rs);
+      const uint64_t nm2 = f2::make(-rs * ln_mean, -rs * ln_mean);
+      const uint64_t zero2 = f2::make(0.f, 0.f);
+      uint64_t st_s = zero2, st_q = zero2;  // STATS: (sum, sumsq) over this warp's columns, in pairs
+      uint64_t dot01 = zero2, dot23 = zero2;  // ROWDOT: tasks 0-1 and 2-3
+
+      auto chunk = [&](const int k, const uint32_t (&r)[32]) {
+        const int c = half + k * kEpiPerQuad;
         const int col0 = n_blk * BN + c * 32;
-        if (col0 >= ep.N) continue;  // warp-uniform
+        if (col0 >= ep.N) return;  // warp-uniform
+        const bool full = col0 + 32 <= ep.N;
+        if constexpr (C::kResidTma) {
+          ptx::mbar_wait(&rfull[rd_buf], (rd_phase >> rd_buf) & 1);
+          rd_phase ^= 1u << rd_buf;
+        }
         float v[32];
-        if constexpr ((EPI & EPI_LNSTATS) != 0) {
-          const float* u = ep.colsum + g * ep.colsum_gstride + col0;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 uu = __ldg(reinterpret_cast<const float4*>(u + j));
-            v[j + 0] = (__uint_as_float(r[j + 0]) - ln_mean * uu.x) * rs;
-            v[j + 1] = (__uint_as_float(r[j + 1]) - ln_mean * uu.y) * rs;
-            v[j + 2] = (__uint_as_float(r[j + 2]) - ln_mean * uu.z) * rs;
-            v[j + 3] = (__uint_as_float(r[j + 3]) - ln_mean * uu.w) * rs;
+        for (int j = 0; j < 32; j += 4) {
+          uint64_t p0 = f2::make(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+          uint64_t p1 = f2::make(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          uint64_t b0 = zero2, b1 = zero2;
+          if constexpr (C::kBiasSmem) {
+            const float4 bb = *reinterpret_cast<const float4*>(cv_bias + k * 32 + j);
+            b0 = f2::make(bb.x, bb.y);
+            b1 = f2::make(bb.z, bb.w);
+          } else if constexpr ((EPI & EPI_BIAS) != 0) {
+            const float* bp = ep.bias + g * ep.bias_gstride + col0 + j;
+            float4 bb;
+            if (full) {
+              bb = __ldg(reinterpret_cast<const float4*>(bp));
+            } else {
+              bb.x = col0 + j + 0 < ep.N ? bp[0] : 0.f;
+              bb.y = col0 + j + 1 < ep.N ? bp[1] : 0.f;
+              bb.z = col0 + j + 2 < ep.N ? bp[2] : 0.f;
+              bb.w = col0 + j + 3 < ep.N ? bp[3] : 0.f;
+            }
+            b0 = f2::make(bb.x, bb.y);
+            b1 = f2::make(bb.z, bb.w);
           }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
-        }
-        epilogue_math<EPI, 32, true>(v, ep, g, row, col0);
-        if constexpr ((EPI & EPI_STATS) != 0) {
-          // padded columns are exactly 0 and add nothing to the sums
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            st_sum += v[j];
-            st_sq = fmaf(v[j], v[j], st_sq);
+          if constexpr ((EPI & EPI_LNSTATS) != 0) {
+            const float4 uu = *reinterpret_cast<const float4*>(cv_u + k * 32 + j);
+            p0 = f2::fma(rs2, p0, f2::fma(nm2, f2::make(uu.x, uu.y), b0));
+            p1 = f2::fma(rs2, p1, f2::fma(nm2, f2::make(uu.z, uu.w), b1));
+          } else if constexpr ((EPI & EPI_ROWSCALE) != 0 && (EPI & EPI_BIAS) != 0) {
+            p0 = f2::fma(p0, rs2, b0);
+            p1 = f2::fma(p1, rs2, b1);
+          } else if constexpr ((EPI & EPI_ROWSCALE) != 0) {
+            p0 = f2::mul(p0, rs2);
+            p1 = f2::mul(p1, rs2);
+          } else if constexpr ((EPI & EPI_BIAS) != 0) {
+            p0 = f2::add(p0, b0);
+            p1 = f2::add(p1, b1);
           }
+          if constexpr ((EPI & EPI_GELU) != 0) {
+            p0 = f2::gelu(p0);
+            p1 = f2::gelu(p1);
+          }
+          if constexpr ((EPI & EPI_RESID) != 0) {
+            float4 rr;
+            if constexpr ((EPI & EPI_RESID_BF16) != 0) {
+              const __nv_bfloat16* rp =
+                  ep.resid_b + g * ep.resid_gstride + static_cast<long long>(row) * ep.resid_ld + col0 + j;
+              if (full) {
+                const uint2 u = *reinterpret_cast<const uint2*>(rp);
+                const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+                const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+                rr = make_float4(lo.x, lo.y, hi.x, hi.y);
+              } else {
+                rr.x = col0 + j + 0 < ep.N ? __bfloat162float(rp[0]) : 0.f;
+                rr.y = col0 + j + 1 < ep.N ? __bfloat162float(rp[1]) : 0.f;
+                rr.z = col0 + j + 2 < ep.N ? __bfloat162float(rp[2]) : 0.f;
+                rr.w = col0 + j + 3 < ep.N ? __bfloat162float(rp[3]) : 0.f;
+              }
+            } else if constexpr (C::kResidTma) {
+              // swizzled (SW128) 32 x 32 fp32 box: 16-byte chunk q of row r at q ^ (r & 7)
+              rr = *reinterpret_cast<const float4*>(rbuf + rd_buf * 4096 + lane * 128 + (((j >> 2) ^ (lane & 7)) << 4));
+            } else {
+              const float* rp = ep.resid + g * ep.resid_gstride + static_cast<long long>(row) * ep.resid_ld + col0 + j;
+              if (full) {
+                rr = *reinterpret_cast<const float4*>(rp);
+              } else {
+                rr.x = col0 + j + 0 < ep.N ? rp[0] : 0.f;
+                rr.y = col0 + j + 1 < ep.N ? rp[1] : 0.f;
+                rr.z = col0 + j + 2 < ep.N ? rp[2] : 0.f;
+                rr.w = col0 + j + 3 < ep.N ? rp[3] : 0.f;
+              }
+            }
+            p0 = f2::add(p0, f2::make(rr.x, rr.y));
+            p1 = f2::add(p1, f2::make(rr.z, rr.w));
+          }
+          if constexpr ((EPI & EPI_STATS) != 0) {
+            // padded columns are exactly 0 and add nothing to the sums
+            st_s = f2::add(st_s, f2::add(p0, p1));
+            st_q = f2::fma(p0, p0, st_q);
+            st_q = f2::fma(p1, p1, st_q);
+          }
+          f2::split(p0, v[j], v[j + 1]);
+          f2::split(p1, v[j + 2], v[j + 3]);
         }
-        if constexpr ((EPI & EPI_ROWDOT) != 0) {
-          // partial dot with dot_w over this chunk (fixed order; cols >= N have dot_w rows
-          // zero-padded by the caller)
-          // dot_w is [N][4] (tasks zero-padded to 4): one broadcast float4 load per column
+        if constexpr (C::kRowDot) {
+          // partial dot with dot_w ([N][4], tasks zero-padded; cols >= N zero rows), fixed order
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float4 w = __ldg(reinterpret_cast<const float4*>(ep.dot_w) + (col0 + j));
-            dot[0] = fmaf(v[j], w.x, dot[0]);
-            dot[1] = fmaf(v[j], w.y, dot[1]);
-            dot[2] = fmaf(v[j], w.z, dot[2]);
-            dot[3] = fmaf(v[j], w.w, dot[3]);
+            const uint64_t vv = f2::make(v[j], v[j]);
+            dot01 = f2::fma(vv, f2::make(w.x, w.y), dot01);
+            dot23 = f2::fma(vv, f2::make(w.z, w.w), dot23);
           }
         } else {
-          if (epi_leader) ptx::tma_store_wait_read<0>();  // staging boxes free again
+          if (epi_leader) ptx::tma_store_wait_read<C::kOutBoxes - 1>();  // this staging box free again
           __syncwarp();
-          stage_row32<kF32>(box, lane, v);
+          uint8_t* ob = box + box_i * C::kOutBoxBytes;
+          if constexpr (C::kOutBoxes > 1) box_i ^= 1;
+          stage_row32<kF32>(ob, lane, v);
           if constexpr (C::kDual) stage_row32<false>(box2, lane, v);
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (epi_leader) {
-            ptx::tma_store_3d(&tmO, box, ep.out_col0 + col0, row0, g);
-            if constexpr (C::kDual) ptx::tma_store_3d(&tmO2, box2, col0, row0, g);
-            ptx::tma_store_commit();
+            if (row0 < ep.M) {
+              ptx::tma_store_3d(&tmO, ob, ep.out_col0 + col0, row0, g);
+              if constexpr (C::kDual) ptx::tma_store_3d(&tmO2, box2, col0, row0, g);
+            }
+            ptx::tma_store_commit();  // one group per chunk keeps the box rotation exact
+          }
+          if constexpr (C::kResidTma) {
+            // the residual box was read before the proxy fence above: refill it
+            ld_issue();
+            rd_buf ^= 1;
           }
         }
+      };
+
+      // TMEM chunks ping-pong between two register sets: the load of chunk k+1
+      // is in flight while chunk k is processed
+      uint32_t ra[32], rb[32];
+      ptx::tmem_ld_32x32b_x32(t_row + half * 32, ra);
+#pragma unroll 1
+      for (int k = 0; k < C::kMyChunks; k += 2) {
+        ptx::tmem_ld_wait();
+        const bool has1 = k + 1 < C::kMyChunks && half + (k + 1) * kEpiPerQuad < kChunks;
+        if (has1) ptx::tmem_ld_32x32b_x32(t_row + (half + (k + 1) * kEpiPerQuad) * 32, rb);
+        chunk(k, ra);
+        if (!has1) break;
+        ptx::tmem_ld_wait();
+        const bool has2 = k + 2 < C::kMyChunks && half + (k + 2) * kEpiPerQuad < kChunks;
+        if (has2) ptx::tmem_ld_32x32b_x32(t_row + (half + (k + 2) * kEpiPerQuad) * 32, ra);
+        chunk(k + 1, rb);
+        if (!has2) break;
       }
       if constexpr ((EPI & EPI_STATS) != 0) {
         if (row0 + lane < ep.M) {
+          float a0, a1, q0, q1;
+          f2::split(st_s, a0, a1);
+          f2::split(st_q, q0, q1);
           float2* dst = reinterpret_cast<float2*>(ep.stats + g * ep.stats_gstride) +
                         static_cast<long long>(row0 + lane) * (kEpiPerQuad * n_tiles) + n_blk * kEpiPerQuad + half;
-          *dst = make_float2(st_sum, st_sq);
+          *dst = make_float2(a0 + a1, q0 + q1);
         }
       }
-      if constexpr ((EPI & EPI_ROWDOT) != 0) {
+      if constexpr (C::kRowDot) {
         if (row0 + lane < ep.M) {
+          float d[4];
+          f2::split(dot01, d[0], d[1]);
+          f2::split(dot23, d[2], d[3]);
           float* dst = reinterpret_cast<float*>(ep.out) +
                        (static_cast<long long>(row0 + lane) * (kEpiPerQuad * n_tiles) + n_blk * kEpiPerQuad + half) * ep.dot_n;
-          for (int t = 0; t < ep.dot_n; ++t) dst[t] = dot[t];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t < ep.dot_n) dst[t] = d[t];
         }
       }
       ptx::tc_fence_before();
@@ -326,6 +544,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (ncl > 1) ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
