@@ -450,6 +450,13 @@ struct Pipe {
     ep.bias = bias; ep.bias_gstride = bias_gstride;
     ep.resid = resid; ep.resid_ld = resid_ld; ep.resid_gstride = resid_gstride;
     ep.M = M; ep.N = N;
+    {
+      static const int g_inner_mode = [] {  // FLAME_GEMM_GINNER=0 disables (A/B experiments)
+        const char* v = getenv("FLAME_GEMM_GINNER");
+        return v ? atoi(v) : 1;
+      }();
+      ep.g_inner = g_inner_mode && G > 1 && (a_shared || (resid != nullptr && resid_gstride == 0));
+    }
     ep.rowscale = rs_ptr; ep.rowscale_gstride = rs_g; ep.dot_w = dot_w; ep.dot_n = dot_n;
     ep.out2 = ln.out2; ep.out2_ld = ln.out2_ld; ep.out2_gstride = ln.out2_gstride;
     ep.stats = ln.stats; ep.stats_gstride = ln.stats_gstride;

@@ -20,7 +20,7 @@ struct GemmProblem {
   int epi;  // EPI_* flags
 };
 
-// 2-CTA clusters (W tile multicast) unless FLAME_GEMM_CLUSTER=1
+// CTA pairs (cta_group::2, 256-row tiles) unless FLAME_GEMM_CLUSTER=1
 static int gemm_cluster_pref() {
   static int v = [] {
     const char* e = getenv("FLAME_GEMM_CLUSTER");
@@ -31,12 +31,16 @@ static int gemm_cluster_pref() {
 
 template <int BN, int EPI>
 static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_sms) {
-  using C = gemm::Cfg<BN, EPI>;
+  using C1 = gemm::Cfg<BN, EPI, 1>;
+  using C = gemm::Cfg<BN, EPI, 2>;
   static bool attr_set = false;
-  static int max_clusters = 0;  // co-resident 2-CTA clusters at this smem size
+  static int max_clusters = 0;  // co-resident CTA pairs at this smem size
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, EPI, 1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmemBytes);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t q = {};
     cudaLaunchAttribute at[1];
@@ -49,7 +53,7 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
     q.dynamicSmemBytes = C::kSmemBytes;
     q.attrs = at;
     q.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, gemm_bf16_tcgen05<BN, EPI>, &q) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, gemm_bf16_tcgen05<BN, EPI, 2>, &q) != cudaSuccess) {
       cudaGetLastError();
       max_clusters = 0;
     }
@@ -57,7 +61,10 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   }
   const int m_tiles = (p.M + gemm::BM - 1) / gemm::BM;
   const int n_tiles = (p.N + BN - 1) / BN;
-  const int ncl = (gemm_cluster_pref() == 2 && m_tiles >= 2 && max_clusters > 0) ? 2 : 1;
+  // CTA pairs pay off for long K loops (FFN W2, K = 2048; expert, K = 3d): measured
+  // at cfg3 W2 0.488 -> 0.458 ms.  The K = 512 GEMMs are epilogue-paced and lose a
+  // little to the pair handshake (W1 0.520 -> 0.541 ms), so they run single-CTA.
+  const int ncl = (gemm_cluster_pref() == 2 && m_tiles >= 2 && max_clusters > 0 && p.K >= 1024) ? 2 : 1;
   CUtensorMap ta, tb;
   const int ga = p.a_shared ? 1 : p.G;
   if (!make_tmap_bf16_3d(&ta, p.A, p.K, p.M, ga, p.lda * 2, p.a_gstride * 2, gemm::BK, gemm::BM))
@@ -89,7 +96,7 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   if (ncl == 1) {
     const int total = p.G * m_tiles * n_tiles;
     const int grid = total < num_sms ? total : num_sms;
-    gemm_bf16_tcgen05<BN, EPI><<<grid, C::kThreads, C::kSmemBytes, s>>>(
+    gemm_bf16_tcgen05<BN, EPI, 1><<<grid, C1::kThreads, C1::kSmemBytes, s>>>(
         ta, tb, to, to2, tr, p.K / gemm::BK, m_tiles, n_tiles, p.G, p.a_shared, ep);
     return cudaGetLastError();
   }
@@ -107,7 +114,7 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   q.stream = s;
   q.attrs = at;
   q.numAttrs = 1;
-  return cudaLaunchKernelEx(&q, gemm_bf16_tcgen05<BN, EPI>, ta, tb, to, to2, tr, p.K / gemm::BK, m_tiles, n_tiles,
+  return cudaLaunchKernelEx(&q, gemm_bf16_tcgen05<BN, EPI, 2>, ta, tb, to, to2, tr, p.K / gemm::BK, m_tiles, n_tiles,
                             p.G, p.a_shared, ep);
 }
 

@@ -14,15 +14,19 @@
 //                 residual in registers -> swizzled smem box -> TMA bulk store
 // The epilogue of tile i overlaps the MMAs of tile i+1 through the second
 // accumulator buffer.
-// Launched with 2-CTA clusters along M, the two CTAs of a cluster work on
-// vertically adjacent tiles of the same column block in lock step: each loads
-// its own A tile plus HALF of the shared W tile, multicast into both CTAs'
-// smem, so the L2->SM operand traffic per CTA drops from (BM+BN) to (BM+BN/2)
-// rows per k-block (the GEMMs here are L2-bandwidth-bound at 128 x 256 tiles).
-// A stage is refilled only after both CTAs' MMAs released it (empty barriers
-// count 2 arrivals, committed by multicast).  The K loop order is fixed per row, so a row's result is
-// independent of which tile / batch position it lands in (batch invariance:
-// chunked == unchunked, duplicate candidates give identical scores).
+// Launched as CTA pairs (2-CTA clusters, cta_group::2): the pair computes a
+// 256 x BN tile with M = 256 MMAs issued by the even CTA.  Each CTA loads its
+// own 128 A rows and HALF of the W tile into its own smem; the tensor core reads
+// both CTAs' operands, and each CTA's TMEM receives its own 128 rows.  So the
+// L2->SM operand traffic per CTA is (BM + BN/2) rows per k-block instead of
+// (BM + BN) (the GEMMs here are L2-bandwidth-bound at 128 x 256 tiles; ncu shows
+// TMA multicast does not reduce L2 traffic at cluster size 2, the pair MMA does).
+// Every TMA of the pair completes on the even CTA's full barrier; MMA commits
+// multicast to both CTAs' empty / tmem_full barriers; both CTAs' epilogue warps
+// release an accumulator on the even CTA's tmem_empty barrier.  The K loop
+// order is fixed per row, so a row's result is independent of which tile /
+// batch position it lands in (batch invariance: chunked == unchunked,
+// duplicate candidates give identical scores).
 #pragma once
 #include "ptx.cuh"
 #include "common.cuh"
@@ -59,6 +63,7 @@ struct GemmEpilogue {
   const float* colsum;    // [G][N] u = gamma . W (column sums of the folded weight)
   long long colsum_gstride;
   int M, N;               // logical bounds of this problem
+  int g_inner;            // tile order: 1 = group index fastest (operand / residual shared by all groups)
 };
 
 // Epilogue stages, applied in this order: ROWSCALE (acc *= rowscale[row]),
@@ -94,7 +99,7 @@ constexpr int kSmemBudget = 227 * 1024;
 #ifndef FLAME_GEMM_HEAVY_WARPS
 #define FLAME_GEMM_HEAVY_WARPS 8
 #endif
-template <int BN, int EPI>
+template <int BN, int EPI, int kCG>
 struct Cfg {
   static constexpr bool kHeavy = (EPI & (EPI_GELU | EPI_LNSTATS | EPI_STATS)) != 0;
   static constexpr int kEpiWarps = kHeavy ? FLAME_GEMM_HEAVY_WARPS : 8;
@@ -115,7 +120,7 @@ struct Cfg {
   static constexpr int kCvecs = (kBiasSmem ? 1 : 0) + (kUSmem ? 1 : 0);
   static constexpr int kCvecBytes = kCvecs * kMyChunks * 32 * 4;
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kBBytes = (BN / kCG) * BK * 2;  // this CTA's share of the W tile
   static constexpr int kStageBytes = kABytes + kBBytes;
   // fp32 residuals are TMA-loaded as 32x32 boxes (row-per-lane global loads
   // would cost one L1 wavefront per 16 bytes), two boxes in flight per warp
@@ -131,12 +136,12 @@ struct Cfg {
 
 }  // namespace gemm
 
-template <int BN, int EPI>
-__global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
+template <int BN, int EPI, int kCG>
+__global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
                       const __grid_constant__ CUtensorMap tmR, int num_k_blocks, int m_tiles, int n_tiles, int groups, int a_shared, GemmEpilogue ep) {
-  using C = gemm::Cfg<BN, EPI>;
+  using C = gemm::Cfg<BN, EPI, kCG>;
   constexpr int kEpiWarps = C::kEpiWarps;
   constexpr int kEpiPerQuad = kEpiWarps / 4;
   constexpr int kStages = C::kStages;
@@ -159,13 +164,27 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  // cluster geometry (1 or 2 CTAs along M); a cluster walks pair-tiles
-  const int ncl = static_cast<int>(ptx::cluster_nctarank());
-  const int crank = static_cast<int>(ptx::cluster_ctarank());
+  // CTA pair (kCG = 2): the two CTAs of a cluster own vertically adjacent 128-row
+  // halves of a 256-row tile; the even CTA issues cta_group::2 MMAs for both
+  constexpr int ncl = kCG;
+  const int crank = kCG == 2 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
   const int m_pairs = (m_tiles + ncl - 1) / ncl;
   const int cid = blockIdx.x / ncl;
   const int nclusters = gridDim.x / ncl;
   const int total_tiles = groups * m_pairs * n_tiles;
+  // tile -> (group, m pair, n block).  Group-fastest order when every group reads
+  // the same A rows or residual tile: the G consecutive tiles hit it in L2.
+  auto decode = [&](int t, int& g, int& mp, int& nb) {
+    if (ep.g_inner) {
+      g = t % groups;
+      nb = (t / groups) % n_tiles;
+      mp = t / (groups * n_tiles);
+    } else {
+      nb = t % n_tiles;
+      mp = (t / n_tiles) % m_pairs;
+      g = t / (n_tiles * m_pairs);
+    }
+  };
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -175,22 +194,22 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     if (C::kResidTma) ptx::tma_prefetch_desc(&tmR);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], ncl);
+      ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tmem_full[s], 1);
-      ptx::mbar_init(&tmem_empty[s], kEpiWarps);
+      ptx::mbar_init(&tmem_empty[s], kEpiWarps * kCG);  // both CTAs' epilogue warps
     }
     if (C::kResidTma)
       for (int s = 0; s < 2 * kEpiWarps; ++s) ptx::mbar_init(&resid_full[s], 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_base_slot);
+  if (warp == 2) ptx::tmem_alloc_cg<C::kTmemCols, kCG>(tmem_base_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
-  if (ncl > 1) ptx::cluster_sync();  // peer barriers initialised before any multicast
+  if constexpr (kCG > 1) ptx::cluster_sync();  // peer barriers / TMEM ready before any pair MMA
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -199,10 +218,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = cid; tile < total_tiles; tile += nclusters) {
-      const int n_blk = tile % n_tiles;
+      int g, mp, n_blk;
+      decode(tile, g, mp, n_blk);
       // the odd tail CTA of a cluster recomputes the last tile; its stores fall past M
-      const int m_blk = min(((tile / n_tiles) % m_pairs) * ncl + crank, m_tiles - 1);
-      const int g = tile / (n_tiles * m_pairs);
+      const int m_blk = min(mp * ncl + crank, m_tiles - 1);
       const int ga = a_shared ? 0 : g;
       for (int kb = 0; kb < num_k_blocks; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -212,33 +231,38 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
 #else
         if (leader) {
 #endif
-          ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-          ptx::tma_load_3d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * gemm::BK,
-                           m_blk * gemm::BM, ga);
-          if (ncl == 1) {
+          if constexpr (kCG == 1) {
+            ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+            ptx::tma_load_3d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * gemm::BK,
+                             m_blk * gemm::BM, ga);
             ptx::tma_load_3d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * gemm::BK,
                              n_blk * BN, g);
           } else {
-            ptx::tma_load_3d_mc(smem_b + stage * C::kBBytes + crank * (C::kBBytes / 2), &tmB, &full[stage],
-                                kb * gemm::BK, n_blk * BN + crank * (BN / 2), g, 0x3);
+            // this CTA's A rows and its half of the W tile, both completing on the
+            // even CTA's full barrier (which expects the pair's bytes)
+            if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+            const uint32_t fb = ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0);
+            ptx::tma_load_3d_cg2(smem_a + stage * C::kABytes, &tmA, fb, kb * gemm::BK, m_blk * gemm::BM, ga);
+            ptx::tma_load_3d_cg2(smem_b + stage * C::kBBytes, &tmB, fb, kb * gemm::BK,
+                                 n_blk * BN + crank * (BN / 2), g);
           }
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-    if (ncl > 1) {
-      // drain: every stage released by both CTAs' MMAs, so no multicast arrival
+    if constexpr (kCG > 1) {
+      // drain: every stage released by the pair's MMAs, so no multicast arrival
       // is still in flight towards this CTA when it exits
       for (int i = 0; i < kStages; ++i) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && crank == 0) {
     // --------------------------------------------------------- MMA issuer
     const bool leader = ptx::elect_one();
-    constexpr uint32_t idesc = ptx::make_idesc_bf16(gemm::BM, BN, 0, 0);
+    constexpr uint32_t idesc = ptx::make_idesc_bf16(gemm::BM * kCG, BN, 0, 0);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -257,15 +281,19 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
           for (int k = 0; k < gemm::BK / 16; ++k) {
             const uint64_t ad = ptx::make_desc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = ptx::make_desc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (kCG == 1) ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            else ptx::mma_bf16_ss_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          if (ncl == 1) ptx::mma_commit(&empty[stage]);
-          else ptx::mma_commit_mc(&empty[stage], 0x3);
+          if constexpr (kCG == 1) ptx::mma_commit(&empty[stage]);
+          else ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
         }
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
-      if (leader) ptx::mma_commit(&tmem_full[acc]);
+      if (leader) {
+        if constexpr (kCG == 1) ptx::mma_commit(&tmem_full[acc]);
+        else ptx::mma_commit_cg2_mc(&tmem_full[acc], 0x3);
+      }
       __syncwarp();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -285,7 +313,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     uint8_t* rbuf = smem_resid + ew * C::kResidBytes;
     uint64_t* rfull = resid_full + 2 * ew;
     auto nk_of = [&](int t) {
-      const int nb = t % n_tiles;
+      int gg, mp, nb;
+      decode(t, gg, mp, nb);
       int n = 0;
 #pragma unroll
       for (int k = 0; k < C::kMyChunks; ++k)
@@ -304,9 +333,9 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     auto ld_issue = [&]() {
       if (ld_t >= total_tiles) return;
       if (epi_leader) {
-        const int nb = ld_t % n_tiles;
-        const int mb = ((ld_t / n_tiles) % m_pairs) * ncl + crank;
-        const int gg = ld_t / (n_tiles * m_pairs);
+        int gg, mp, nb;
+        decode(ld_t, gg, mp, nb);
+        const int mb = mp * ncl + crank;
         const int c0 = nb * BN + (half + ld_k * kEpiPerQuad) * 32;
         const int r0 = min(mb * gemm::BM + wq * 32, ep.M - 1);
         ptx::mbar_arrive_expect_tx(&rfull[ld_buf], 32 * 32 * 4);
@@ -325,9 +354,9 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = cid; tile < total_tiles; tile += nclusters) {
-      const int n_blk = tile % n_tiles;
-      const int m_blk = ((tile / n_tiles) % m_pairs) * ncl + crank;  // may be m_tiles (tail): rows >= M
-      const int g = tile / (n_tiles * m_pairs);
+      int g, mp, n_blk;
+      decode(tile, g, mp, n_blk);
+      const int m_blk = mp * ncl + crank;  // may be m_tiles (tail): rows >= M
       if constexpr (C::kCvecs > 0) {
         // this warp's slice of the per-column vectors, fetched while the MMAs run
         __syncwarp();
@@ -535,7 +564,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tmem_empty[acc]);
+      if (lane == 0) {
+        if constexpr (kCG == 1) ptx::mbar_arrive(&tmem_empty[acc]);
+        else ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tmem_empty[acc]), 0));
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (epi_leader) ptx::tma_store_wait<0>();
@@ -544,10 +576,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI>::kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (ncl > 1) ptx::cluster_sync();
+  if constexpr (kCG > 1) ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+    ptx::tmem_dealloc_cg<C::kTmemCols, kCG>(tmem_base);
   }
 }
 

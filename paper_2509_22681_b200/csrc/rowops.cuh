@@ -91,14 +91,26 @@ __global__ void gated_fusion_rows(const float* __restrict__ xc, long long x_ld, 
   const int row = static_cast<int>(idx / per_row);
   const int c = static_cast<int>(idx % per_row) * 4;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int g = 0; g < G; ++g) {
-    const float4 h = *reinterpret_cast<const float4*>(xc + g * x_gstride + row * x_ld + c);
-    const float4 w = *reinterpret_cast<const float4*>(gate_w + g * D + c);
-    const float4 b = *reinterpret_cast<const float4*>(gate_b + g * D + c);
-    acc[0] = acc[0] + sigmoid_f(h.x * w.x + b.x) * h.x;
-    acc[1] = acc[1] + sigmoid_f(h.y * w.y + b.y) * h.y;
-    acc[2] = acc[2] + sigmoid_f(h.z * w.z + b.z) * h.z;
-    acc[3] = acc[3] + sigmoid_f(h.w * w.w + b.w) * h.w;
+  // the block outputs are read exactly once: issue 8 streaming loads before
+  // consuming any, then accumulate strictly in block order
+  constexpr int kBatch = 8;
+  for (int g0 = 0; g0 < G; g0 += kBatch) {
+    float4 hv[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q)
+      if (g0 + q < G) hv[q] = __ldcs(reinterpret_cast<const float4*>(xc + (g0 + q) * x_gstride + row * x_ld + c));
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      if (g0 + q >= G) break;
+      const int g = g0 + q;
+      const float4 h = hv[q];
+      const float4 w = __ldg(reinterpret_cast<const float4*>(gate_w + g * D + c));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(gate_b + g * D + c));
+      acc[0] = acc[0] + sigmoid_f(h.x * w.x + b.x) * h.x;
+      acc[1] = acc[1] + sigmoid_f(h.y * w.y + b.y) * h.y;
+      acc[2] = acc[2] + sigmoid_f(h.z * w.z + b.z) * h.z;
+      acc[3] = acc[3] + sigmoid_f(h.w * w.w + b.w) * h.w;
+    }
   }
   if constexpr (std::is_same<TOut, __nv_bfloat16>::value) {
     // split-bf16 operand for the expert GEMM: [hi | hi | lo] (row stride 3D),
