@@ -441,6 +441,8 @@ struct Pipe {
   double flop_div = 1.0;  // split-bf16 GEMMs do 3x the algorithmic FLOPs
   GemmEpilogue ln{};      // folded-LN2 producer / consumer operands (reset after use)
   const __nv_bfloat16* resid_b = nullptr;  // bf16 residual of the next gemm()
+  const float* gate_w = nullptr;           // gated-fusion vectors of the next gemm() (EPI_GATED)
+  const float* gate_b = nullptr;
   int gemm(const Act* A, long long lda, long long a_gstride, int a_shared, const Act* W, long long ldw,
            long long w_gstride, int M, int N, int K, int G, void* out, long long out_ld,
            long long out_gstride, int out_col0, const float* bias, long long bias_gstride,
@@ -462,14 +464,18 @@ struct Pipe {
     ep.stats = ln.stats; ep.stats_gstride = ln.stats_gstride;
     ep.lnstats = ln.lnstats; ep.lnstats_gstride = ln.lnstats_gstride; ep.stats_parts = ln.stats_parts;
     ep.d_true = ln.d_true; ep.colsum = ln.colsum; ep.colsum_gstride = ln.colsum_gstride;
-    ep.resid_b = resid_b;
+    ep.resid_b = resid_b; ep.gate_w = gate_w; ep.gate_b = gate_b;
     rs_ptr = nullptr; rs_g = 0; dot_w = nullptr; dot_n = 0; ln = GemmEpilogue{}; resid_b = nullptr;
+    gate_w = nullptr; gate_b = nullptr;
     if (M <= 0) return 0;
     {
       const double ab = sizeof(Act);
       const double ob = (epi & EPI_OUT_F32) || !std::is_same<Act, __nv_bfloat16>::value ? 4.0 : 2.0;
-      const double byts = static_cast<double>(G) * (static_cast<double>(M) * K * ab + static_cast<double>(N) * K * ab +
-                                                    static_cast<double>(M) * N * (ob + ((epi & EPI_RESID) ? 4.0 : 0.0)));
+      double byts = static_cast<double>(G) * (static_cast<double>(M) * K * ab + static_cast<double>(N) * K * ab +
+                                              static_cast<double>(M) * N * (ob + ((epi & EPI_RESID) ? 4.0 : 0.0)));
+      if (epi & EPI_GATED)  // bf16 residual in, one [M][3N] bf16 fused operand out
+        byts = static_cast<double>(G) * (static_cast<double>(M) * K * ab + static_cast<double>(N) * K * ab +
+                                         static_cast<double>(M) * N * 2.0) + static_cast<double>(M) * 3 * N * 2.0;
       mark(gemm_name, 2.0 * G * static_cast<double>(M) * N * K / flop_div, byts);
       flop_div = 1.0;
     }
@@ -664,6 +670,11 @@ struct Pipe {
     Act* Hf = act(e->Hf);
     float* RS = e->RS;
     float* Xcur = nullptr;  // residual stream input of this layer (null at layer 0)
+    static const bool fuse_gate = [] {  // FLAME_FUSE_GATE=0: separate gated-fusion pass (A/B)
+      const char* v = getenv("FLAME_FUSE_GATE");
+      return !(v && atoi(v) == 0);
+    }();
+    bool gated_done = false;
     for (int l = 0; l < c->L; ++l) {
       const LayerW& w = c->layers[l];
       const bool last = l == c->L - 1;
@@ -753,7 +764,16 @@ struct Pipe {
                           Hf + r0 * F, F, gF, 0, w.b1, F, nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
       }
       gemm_name = "gemm_ffn_w2";
-      if constexpr (kFold) {
+      if (kFold && last && fuse_gate) {
+        // last layer: the W2 epilogue also performs the gated fusion over blocks
+        // (forward.py:143-156) and writes only the split-bf16 expert operand
+        resid_b = reinterpret_cast<const __nv_bfloat16*>(Y) + r0 * D;
+        gate_w = c->gate_w; gate_b = c->gate_b;
+        if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F,
+                          G, e->Fz, kSplitK * D, 0, 0, w.b2, D, nullptr, D, gD,
+                          EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_GATED)) return rc;
+        gated_done = true;
+      } else if constexpr (kFold) {
         resid_b = reinterpret_cast<const __nv_bfloat16*>(Y) + r0 * D;
         if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F,
                           G, Xnext + r0 * D, D, gD, 0, w.b2, D, nullptr, D, gD,
@@ -766,7 +786,7 @@ struct Pipe {
       Xcur = Xnext;
     }
     // gated fusion over blocks (forward.py:143-156)
-    {
+    if (!gated_done) {
       const long long n = Rc * (D / 4);
       mark("gated_fusion", 0.0, static_cast<double>(Rc) * D * (4.0 * G + kSplitK * sizeof(Act)));
       gated_fusion_rows<Act><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(

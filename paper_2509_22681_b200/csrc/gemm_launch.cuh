@@ -76,17 +76,23 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   if constexpr ((EPI & EPI_ROWDOT) != 0) {
     // row-dot epilogue writes its partials directly; the map is a valid placeholder
     if (!make_tmap_out_3d(&to, p.ep.out, 4, 32, p.M, 1, 128, 0)) return cudaErrorInvalidValue;
+  } else if constexpr (C::kGated) {
+    // one [M][3N] bf16 output (hi | hi | lo) shared by all groups
+    if (!make_tmap_out_3d(&to, p.ep.out, 2, 3ull * p.N, p.M, 1, p.ep.out_ld * 2, 0)) return cudaErrorInvalidValue;
   } else if (!make_tmap_out_3d(&to, p.ep.out, ob, static_cast<uint64_t>(p.ep.out_col0) + p.N, p.M, p.G,
                                p.ep.out_ld * ob, p.ep.out_gstride * ob)) {
     return cudaErrorInvalidValue;
   }
   CUtensorMap to2 = to, tr = to;
   if constexpr (C::kResidTma) {
-    if (!make_tmap_out_3d(&tr, const_cast<float*>(p.ep.resid), 4, p.N, p.M, p.ep.resid_gstride ? p.G : 1,
-                          p.ep.resid_ld * 4, p.ep.resid_gstride * 4))
+    constexpr int rb = (EPI & EPI_RESID_BF16) ? 2 : 4;
+    void* rbase = (EPI & EPI_RESID_BF16) ? const_cast<__nv_bfloat16*>(p.ep.resid_b)
+                                         : static_cast<void*>(const_cast<float*>(p.ep.resid));
+    if (!make_tmap_out_3d(&tr, rbase, rb, p.N, p.M, p.ep.resid_gstride ? p.G : 1, p.ep.resid_ld * rb,
+                          p.ep.resid_gstride * rb))
       return cudaErrorInvalidValue;
   }
-  if constexpr (C::kDual) {
+  if constexpr (C::kDual && !C::kGated) {
     if (!make_tmap_out_3d(&to2, p.ep.out2, 2, p.N, p.M, p.G, p.ep.out2_ld * 2, p.ep.out2_gstride * 2))
       return cudaErrorInvalidValue;
   }
@@ -156,6 +162,11 @@ static int gemm_row_parts(int N, int epi) {
 
 static cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t s, int num_sms) {
   if (p.K % gemm::BK != 0 || p.M < 1 || p.N < 1 || p.G < 1) return cudaErrorInvalidValue;
+  constexpr int kGatedW2 = EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_GATED;
+  if (p.epi & EPI_GATED) {
+    if (p.epi != kGatedW2 || p.N % 32 != 0) return cudaErrorInvalidValue;
+    return launch_gemm_t<128, kGatedW2>(p, s, num_sms);
+  }
   if (p.N >= 256) return launch_gemm_bn<256>(p, s, num_sms);
   return launch_gemm_bn<128>(p, s, num_sms);
 }

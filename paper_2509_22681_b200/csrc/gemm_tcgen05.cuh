@@ -62,6 +62,12 @@ struct GemmEpilogue {
   int d_true;
   const float* colsum;    // [G][N] u = gamma . W (column sums of the folded weight)
   long long colsum_gstride;
+  // EPI_GATED (FFN W2 of the last layer + gated fusion): per group g the tile's
+  // X2 = acc + b2 + X1 is folded into sum_g sigmoid(X2 * gate_w[g] + gate_b[g]) * X2
+  // (kept in TMEM across the groups, which one CTA walks in order); only the sum
+  // reaches HBM, as the split-bf16 [hi | hi | lo] expert operand ([M][3N] bf16)
+  const float* gate_w;    // [G][N]
+  const float* gate_b;    // [G][N]
   int M, N;               // logical bounds of this problem
   int g_inner;            // tile order: 1 = group index fastest (operand / residual shared by all groups)
 };
@@ -80,6 +86,7 @@ enum : int {
   EPI_STATS = 64,
   EPI_LNSTATS = 128,
   EPI_RESID_BF16 = 256,
+  EPI_GATED = 512,
 };
 
 namespace gemm {
@@ -107,8 +114,12 @@ struct Cfg {
   static constexpr int kThreads = 128 + 32 * kEpiWarps;
   static constexpr bool kF32 = (EPI & EPI_OUT_F32) != 0;
   static constexpr bool kRowDot = (EPI & EPI_ROWDOT) != 0;
-  // STATS with an fp32 primary output also emits a bf16 copy (second TMA store)
-  static constexpr bool kDual = (EPI & EPI_STATS) != 0 && kF32;
+  static constexpr bool kGated = (EPI & EPI_GATED) != 0;
+  static_assert(!kGated || (BN == 128 && !kF32 && (EPI & EPI_RESID_BF16) != 0),
+                "gated-fusion epilogue: BN = 128, bf16 output, bf16 residual");
+  // STATS with an fp32 primary output, and the gated sum (hi + lo halves), also
+  // stage a second bf16 box
+  static constexpr bool kDual = ((EPI & EPI_STATS) != 0 && kF32) || kGated;
   static constexpr int kOutBoxes = 1;
   static constexpr int kOutBoxBytes = kRowDot ? 0 : 32 * 32 * (kF32 ? 4 : 2);
   static constexpr int kBoxBytes = kOutBoxes * kOutBoxBytes + (kDual ? 32 * 32 * 2 : 0);
@@ -117,20 +128,23 @@ struct Cfg {
   static constexpr int kMyChunks = (kChunks + kEpiPerQuad - 1) / kEpiPerQuad;
   static constexpr bool kBiasSmem = (EPI & EPI_BIAS) != 0 && !kF32;
   static constexpr bool kUSmem = (EPI & EPI_LNSTATS) != 0;
-  static constexpr int kCvecs = (kBiasSmem ? 1 : 0) + (kUSmem ? 1 : 0);
+  static constexpr int kCvecs = (kBiasSmem ? 1 : 0) + (kUSmem ? 1 : 0) + (kGated ? 2 : 0);
   static constexpr int kCvecBytes = kCvecs * kMyChunks * 32 * 4;
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = (BN / kCG) * BK * 2;  // this CTA's share of the W tile
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // fp32 residuals are TMA-loaded as 32x32 boxes (row-per-lane global loads
-  // would cost one L1 wavefront per 16 bytes), two boxes in flight per warp
-  static constexpr bool kResidTma = (EPI & EPI_RESID) != 0 && (EPI & EPI_RESID_BF16) == 0;
-  static constexpr int kResidBytes = kResidTma ? 2 * 32 * 32 * 4 : 0;
+  // residuals are TMA-loaded as 32x32 boxes (fp32: SW128, bf16: SW64; row-per-lane
+  // global loads would cost one L1 wavefront per 16 bytes and expose their full
+  // latency in every chunk), two boxes in flight per warp
+  static constexpr bool kResidTma = (EPI & EPI_RESID) != 0;
+  static constexpr int kResidBox = 32 * 32 * ((EPI & EPI_RESID_BF16) != 0 ? 2 : 4);
+  static constexpr int kResidBytes = kResidTma ? 2 * kResidBox : 0;
   static constexpr int kFixed = kEpiWarps * (kBoxBytes + kCvecBytes + kResidBytes) + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int kStagesFit = (kSmemBudget - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
   static_assert(kStages >= 2, "GEMM smem ring too shallow");
-  static constexpr int kTmemCols = 2 * BN;
+  // two accumulators (+ the gated running sum at columns [2 BN, 3 BN))
+  static constexpr int kTmemCols = kGated ? 512 : 2 * BN;
   static constexpr int kSmemBytes = kStages * kStageBytes + kFixed;
 };
 
@@ -175,7 +189,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   // tile -> (group, m pair, n block).  Group-fastest order when every group reads
   // the same A rows or residual tile: the G consecutive tiles hit it in L2.
   auto decode = [&](int t, int& g, int& mp, int& nb) {
-    if (ep.g_inner) {
+    if (C::kGated || ep.g_inner) {
       g = t % groups;
       nb = (t / groups) % n_tiles;
       mp = t / (groups * n_tiles);
@@ -183,6 +197,16 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       nb = t % n_tiles;
       mp = (t / n_tiles) % m_pairs;
       g = t / (n_tiles * m_pairs);
+    }
+  };
+  // the it-th tile of this cluster (>= total_tiles when done).  Gated fusion: a
+  // cluster owns whole (m pair, n block) super tiles and walks their groups in order
+  auto tile_at = [&](int it) -> int {
+    if constexpr (C::kGated) {
+      const int st = cid + (it / groups) * nclusters;
+      return st < m_pairs * n_tiles ? st * groups + it % groups : total_tiles;
+    } else {
+      return cid + it * nclusters;
     }
   };
 
@@ -217,7 +241,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     const bool leader = ptx::elect_one();
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = cid; tile < total_tiles; tile += nclusters) {
+    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int g, mp, n_blk;
       decode(tile, g, mp, n_blk);
       // the odd tail CTA of a cluster recomputes the last tile; its stores fall past M
@@ -267,7 +291,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cid; tile < total_tiles; tile += nclusters) {
+    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -321,12 +345,12 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         n += (half + k * kEpiPerQuad < kChunks && nb * BN + (half + k * kEpiPerQuad) * 32 < ep.N) ? 1 : 0;
       return n;
     };
-    int ld_t = cid, ld_k = 0, ld_buf = 0, rd_buf = 0;
+    int ld_it = 0, ld_t = tile_at(0), ld_k = 0, ld_buf = 0, rd_buf = 0;
     uint32_t rd_phase = 0;  // bit b: parity of buffer b's next completion
     auto ld_advance = [&](bool step) {
       if (step) ++ld_k;
       while (ld_t < total_tiles && ld_k >= nk_of(ld_t)) {
-        ld_t += nclusters;
+        ld_t = tile_at(++ld_it);
         ld_k = 0;
       }
     };
@@ -338,8 +362,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         const int mb = mp * ncl + crank;
         const int c0 = nb * BN + (half + ld_k * kEpiPerQuad) * 32;
         const int r0 = min(mb * gemm::BM + wq * 32, ep.M - 1);
-        ptx::mbar_arrive_expect_tx(&rfull[ld_buf], 32 * 32 * 4);
-        ptx::tma_load_3d(rbuf + ld_buf * 4096, &tmR, &rfull[ld_buf], c0, r0, ep.resid_gstride ? gg : 0);
+        ptx::mbar_arrive_expect_tx(&rfull[ld_buf], C::kResidBox);
+        ptx::tma_load_3d(rbuf + ld_buf * C::kResidBox, &tmR, &rfull[ld_buf], c0, r0, ep.resid_gstride ? gg : 0);
       }
       ld_buf ^= 1;
       ld_advance(true);
@@ -351,9 +375,11 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     }
     float* cv_bias = reinterpret_cast<float*>(smem_cvec + ew * C::kCvecBytes);
     float* cv_u = cv_bias + (C::kBiasSmem ? C::kMyChunks * 32 : 0);
+    float* cv_gw = cv_u + (C::kUSmem ? C::kMyChunks * 32 : 0);
+    float* cv_gb = cv_gw + (C::kGated ? C::kMyChunks * 32 : 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cid; tile < total_tiles; tile += nclusters) {
+    for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int g, mp, n_blk;
       decode(tile, g, mp, n_blk);
       const int m_blk = mp * ncl + crank;  // may be m_tiles (tail): rows >= M
@@ -366,6 +392,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
           const bool ok = half + k * kEpiPerQuad < kChunks && col < ep.N;
           if constexpr (C::kBiasSmem) cv_bias[k * 32 + lane] = ok ? __ldg(ep.bias + g * ep.bias_gstride + col) : 0.f;
           if constexpr (C::kUSmem) cv_u[k * 32 + lane] = ok ? __ldg(ep.colsum + g * ep.colsum_gstride + col) : 0.f;
+          if constexpr (C::kGated) {
+            cv_gw[k * 32 + lane] = ok ? __ldg(ep.gate_w + g * ep.N + col) : 0.f;
+            cv_gb[k * 32 + lane] = ok ? __ldg(ep.gate_b + g * ep.N + col) : 0.f;
+          }
         }
         __syncwarp();
       }
@@ -375,6 +405,9 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       // rows past M are clipped by the TMA store; clamp their residual reads
       const int row = min(row0 + lane, ep.M - 1);
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
+      // gated fusion: running sum over groups at TMEM columns [2 BN, 3 BN)
+      const uint32_t t_gsum = tmem_base + 2 * BN + (static_cast<uint32_t>(wq * 32) << 16);
+      const bool g_first = g == 0, g_last = g == groups - 1;
       float rs = (EPI & EPI_ROWSCALE) ? ep.rowscale[g * ep.rowscale_gstride + row] : 1.f;
       float ln_mean = 0.f;
       if constexpr ((EPI & EPI_LNSTATS) != 0) {
@@ -407,6 +440,13 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
           rd_phase ^= 1u << rd_buf;
         }
         float v[32];
+        uint32_t gs[32];  // gated running sum of this chunk (groups < g)
+        if constexpr (C::kGated) {
+          if (!g_first) {
+            ptx::tmem_ld_32x32b_x32(t_gsum + c * 32, gs);
+            ptx::tmem_ld_wait();
+          }
+        }
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           uint64_t p0 = f2::make(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
@@ -450,7 +490,14 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
           }
           if constexpr ((EPI & EPI_RESID) != 0) {
             float4 rr;
-            if constexpr ((EPI & EPI_RESID_BF16) != 0) {
+            if constexpr (C::kResidTma && (EPI & EPI_RESID_BF16) != 0) {
+              // SW64 32 x 32 bf16 box: 16-byte chunk q of row r at q ^ ((r >> 1) & 3)
+              const uint2 u = *reinterpret_cast<const uint2*>(
+                  rbuf + rd_buf * C::kResidBox + lane * 64 + ((((j >> 3) ^ ((lane >> 1) & 3))) << 4) + (j & 4) * 2);
+              const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+              const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+              rr = make_float4(lo.x, lo.y, hi.x, hi.y);
+            } else if constexpr ((EPI & EPI_RESID_BF16) != 0) {
               const __nv_bfloat16* rp =
                   ep.resid_b + g * ep.resid_gstride + static_cast<long long>(row) * ep.resid_ld + col0 + j;
               if (full) {
@@ -466,7 +513,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
               }
             } else if constexpr (C::kResidTma) {
               // swizzled (SW128) 32 x 32 fp32 box: 16-byte chunk q of row r at q ^ (r & 7)
-              rr = *reinterpret_cast<const float4*>(rbuf + rd_buf * 4096 + lane * 128 + (((j >> 2) ^ (lane & 7)) << 4));
+              rr = *reinterpret_cast<const float4*>(rbuf + rd_buf * C::kResidBox + lane * 128 + (((j >> 2) ^ (lane & 7)) << 4));
             } else {
               const float* rp = ep.resid + g * ep.resid_gstride + static_cast<long long>(row) * ep.resid_ld + col0 + j;
               if (full) {
@@ -480,6 +527,22 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
             }
             p0 = f2::add(p0, f2::make(rr.x, rr.y));
             p1 = f2::add(p1, f2::make(rr.z, rr.w));
+          }
+          if constexpr (C::kGated) {
+            // forward.py:153-156: fused += sigmoid(h * w_g + c_g) * h, in block order
+            const float4 gw = *reinterpret_cast<const float4*>(cv_gw + k * 32 + j);
+            const float4 gb = *reinterpret_cast<const float4*>(cv_gb + k * 32 + j);
+            const uint64_t z0 = f2::fma(p0, f2::make(gw.x, gw.y), f2::make(gb.x, gb.y));
+            const uint64_t z1 = f2::fma(p1, f2::make(gw.z, gw.w), f2::make(gb.z, gb.w));
+            float a0, a1, a2, a3;
+            f2::split(z0, a0, a1);
+            f2::split(z1, a2, a3);
+            p0 = f2::mul(p0, f2::make(sigmoid_fast(a0), sigmoid_fast(a1)));
+            p1 = f2::mul(p1, f2::make(sigmoid_fast(a2), sigmoid_fast(a3)));
+            if (!g_first) {
+              p0 = f2::add(f2::make(__uint_as_float(gs[j]), __uint_as_float(gs[j + 1])), p0);
+              p1 = f2::add(f2::make(__uint_as_float(gs[j + 2]), __uint_as_float(gs[j + 3])), p1);
+            }
           }
           if constexpr ((EPI & EPI_STATS) != 0) {
             // padded columns are exactly 0 and add nothing to the sums
@@ -499,27 +562,59 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
             dot01 = f2::fma(vv, f2::make(w.x, w.y), dot01);
             dot23 = f2::fma(vv, f2::make(w.z, w.w), dot23);
           }
+        } else if (C::kGated && !g_last) {
+          // carry the running sum to the next group's tile (same thread, same lanes)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) gs[j] = __float_as_uint(v[j]);
+          ptx::tmem_st_32x32b_x16(t_gsum + c * 32, *reinterpret_cast<const uint32_t(*)[16]>(gs));
+          ptx::tmem_st_32x32b_x16(t_gsum + c * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(gs + 16));
+          ptx::tmem_st_wait();
         } else {
           if (epi_leader) ptx::tma_store_wait_read<C::kOutBoxes - 1>();  // this staging box free again
           __syncwarp();
           uint8_t* ob = box + box_i * C::kOutBoxBytes;
           if constexpr (C::kOutBoxes > 1) box_i ^= 1;
-          stage_row32<kF32>(ob, lane, v);
-          if constexpr (C::kDual) stage_row32<false>(box2, lane, v);
+          if constexpr (C::kGated) {
+            // split-bf16 expert operand: hi = bf16(sum), lo = bf16(sum - hi)
+            float lo[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float hi = __bfloat162float(__float2bfloat16_rn(v[j]));
+              lo[j] = v[j] - hi;
+              v[j] = hi;
+            }
+            stage_row32<false>(ob, lane, v);
+            stage_row32<false>(box2, lane, lo);
+          } else {
+            stage_row32<kF32>(ob, lane, v);
+            if constexpr (C::kDual) stage_row32<false>(box2, lane, v);
+          }
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (epi_leader) {
             if (row0 < ep.M) {
-              ptx::tma_store_3d(&tmO, ob, ep.out_col0 + col0, row0, g);
-              if constexpr (C::kDual) ptx::tma_store_3d(&tmO2, box2, col0, row0, g);
+              if constexpr (C::kGated) {
+                // [hi | hi | lo], one group of 3N columns
+                ptx::tma_store_3d(&tmO, ob, col0, row0, 0);
+                ptx::tma_store_3d(&tmO, ob, ep.N + col0, row0, 0);
+                ptx::tma_store_3d(&tmO, box2, 2 * ep.N + col0, row0, 0);
+              } else {
+                ptx::tma_store_3d(&tmO, ob, ep.out_col0 + col0, row0, g);
+                if constexpr (C::kDual) ptx::tma_store_3d(&tmO2, box2, col0, row0, g);
+              }
             }
             ptx::tma_store_commit();  // one group per chunk keeps the box rotation exact
           }
-          if constexpr (C::kResidTma) {
-            // the residual box was read before the proxy fence above: refill it
-            ld_issue();
-            rd_buf ^= 1;
+        }
+        if constexpr (C::kResidTma) {
+          // the residual box was read before a proxy fence (the store path's, or
+          // this one): refill it with the next box of the stream
+          if (C::kGated && !g_last) {
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
           }
+          ld_issue();
+          rd_buf ^= 1;
         }
       };
 
