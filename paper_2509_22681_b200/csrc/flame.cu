@@ -623,19 +623,29 @@ struct Pipe {
       PdaGatherArgs g{};
       g.l = l; g.table = c->table; g.num_items = c->num_items; g.D = c->D; g.d_true = c->d; g.G = c->G;
       g.hb_bkt = e->hb_bkt; g.o = assemble_out();
-      int bx = (c->num_sms * 8 + 2 * e->R - 1) / (2 * e->R);
-      if (bx < 1) bx = 1;
-      const int max_bx = (e->cap + 7) / 8;
-      if (bx > max_bx) bx = max_bx < 1 ? 1 : max_bx;
-      dim3 grid(bx, 2 * e->R);
+      // one warp per unique id, plus one per padding row (together <= 2 x capacity)
+      dim3 grid(static_cast<unsigned>((2 * e->cap + 7) / 8), 2 * e->R);
       // rows out + table rows read (upper bound: one per position); candidates also get fp32
       const double tab = c->table_dtype == FLAME_TABLE_BF16 ? 2.0 : 4.0;
       mark("pda_gather", 0.0, static_cast<double>(e->R) * c->D *
                                   (e->H_bkt * (tab + row_bytes) + e->c_bkt * (tab + 4.0 + (e->Ecc ? 2.0 : 0.0))));
-      if (c->table_dtype == FLAME_TABLE_BF16)
-        pda_gather<__nv_bfloat16><<<grid, 256, 0, s>>>(g);
-      else
-        pda_gather<float><<<grid, 256, 0, s>>>(g);
+      const int chunks = (c->D + 127) / 128;
+#define PDA_GATHER(T, K) pda_gather<T, K><<<grid, 256, 0, s>>>(g)
+#define PDA_GATHER_T(T)                                                   \
+  switch (chunks) {                                                       \
+    case 1: PDA_GATHER(T, 1); break;                                      \
+    case 2: PDA_GATHER(T, 2); break;                                      \
+    case 3: case 4: PDA_GATHER(T, 4); break;                              \
+    case 5: case 6: PDA_GATHER(T, 6); break;                              \
+    default: PDA_GATHER(T, 8); break;                                     \
+  }
+      if (c->table_dtype == FLAME_TABLE_BF16) {
+        PDA_GATHER_T(__nv_bfloat16)
+      } else {
+        PDA_GATHER_T(float)
+      }
+#undef PDA_GATHER_T
+#undef PDA_GATHER
       if (int rc = check()) return rc;
     }
     return 0;

@@ -151,40 +151,41 @@ struct PdaGatherArgs {
   AssembleOut o;  // fp32 rows (optional) + centered bf16 rows + rstd (folded LN1)
 };
 
+template <int kChunks>
 __device__ __forceinline__ void assemble_row_st(const AssembleOut& o, bool hist, long long row,
-                                                const float4 (&v)[8], int lane, int D, int d_true,
+                                                const float4 (&v)[kChunks], int lane, int D, int d_true,
                                                 RowStats st) {
   float* f = hist ? o.Eh : o.Ec;
   if (f != nullptr) {
     float* dst = f + row * D;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kChunks; ++k) {
       const int c = (k * 32 + lane) * 4;
       if (c < D) *reinterpret_cast<float4*>(dst + c) = v[k];
     }
   }
   __nv_bfloat16* y = hist ? o.Ehc : o.Ecc;
   if (y != nullptr) {
-    store_centered<8>(y + row * D, v, st.mean, lane, D, d_true);
+    store_centered<kChunks>(y + row * D, v, st.mean, lane, D, d_true);
     if (lane == 0) (hist ? o.rs_h : o.rs_c)[row] = st.rstd;
   }
 }
 
-template <typename TTab>
-__global__ void pda_gather(PdaGatherArgs a) {
-  constexpr int kMaxChunks = 8;  // D <= 32 lanes * 4 * 8 = 1024
+// One warp per unique id of a list (grid.x covers the list capacity twice: warps
+// past the unique count zero the list's padding rows).  The warp reads the id's
+// table row once, computes its LayerNorm statistics once, then fetches the run's
+// destination positions 32 at a time (one coalesced load) and writes the row to
+// each.  kChunks = D / 128 float4 per lane keeps registers low enough for 8
+// resident CTAs per SM: the kernel is memory-latency bound.
+template <typename TTab, int kChunks>
+__global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
   const int list = blockIdx.y;
   const bool is_hist = list < a.l.R;
   const int r = is_hist ? list : list - a.l.R;
   const int n = is_hist ? a.l.hist_len[r] : a.l.cand_len[r];
   const int nu = a.l.n_unique[list];
   const int lane = threadIdx.x % 32;
-  const int warps_per_grid_x = gridDim.x * (blockDim.x / 32);
-  const int wid = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const long long* uq = a.l.unique + static_cast<long long>(list) * a.l.cap;
-  const int* sp = a.l.spos + static_cast<long long>(list) * a.l.cap;
-  const int* us = a.l.ustart + static_cast<long long>(list) * a.l.cap;
-  const TTab* table = reinterpret_cast<const TTab*>(a.table);
+  const int u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int hb = is_hist ? n / a.G : 0;
   auto row_of = [&](int p) -> long long {  // destination row of list position p
     if (is_hist) {
@@ -193,37 +194,48 @@ __global__ void pda_gather(PdaGatherArgs a) {
     }
     return static_cast<long long>(r) * a.l.C_bkt + p;
   };
-  for (int u = wid; u < nu; u += warps_per_grid_x) {
+  if (u < nu) {
+    const long long* uq = a.l.unique + static_cast<long long>(list) * a.l.cap;
+    const int* sp = a.l.spos + static_cast<long long>(list) * a.l.cap;
+    const int* us = a.l.ustart + static_cast<long long>(list) * a.l.cap;
     const long long id = uq[u];
-    const bool known = id >= 0 && id < a.num_items;
-    float4 v[kMaxChunks];
-#pragma unroll
-    for (int k = 0; k < kMaxChunks; ++k) {
-      const int c = (k * 32 + lane) * 4;
-      v[k] = (known && c < a.D) ? load_row4<TTab>(table + id * a.D, c) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    // the row is read once; its LayerNorm statistics are computed once per unique id
-    const RowStats st = warp_row_stats<kMaxChunks>(v, lane, a.D, a.d_true);
     const int b = us[u];
     const int e = (u + 1 < nu) ? us[u + 1] : n;
-    for (int k = b; k < e; ++k) assemble_row_st(a.o, is_hist, row_of(sp[k]), v, lane, a.D, a.d_true, st);
+    const bool known = id >= 0 && id < a.num_items;
+    const TTab* table = reinterpret_cast<const TTab*>(a.table) + (known ? id : 0) * a.D;
+    float4 v[kChunks];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+      const int c = (k * 32 + lane) * 4;
+      v[k] = (known && c < a.D) ? load_row4<TTab>(table, c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    int pos = b + lane < e ? sp[b + lane] : 0;  // first 32 positions of the run, in flight with the row
+    const RowStats st = warp_row_stats<kChunks>(v, lane, a.D, a.d_true);
+    for (int k0 = b; k0 < e; k0 += 32) {
+      if (k0 != b) pos = k0 + lane < e ? sp[k0 + lane] : 0;
+      const int cnt = min(32, e - k0);
+      for (int j = 0; j < cnt; ++j)
+        assemble_row_st<kChunks>(a.o, is_hist, row_of(__shfl_sync(0xffffffffu, pos, j)), v, lane, a.D,
+                                 a.d_true, st);
+    }
+    return;
   }
   // zero the padding rows of this list's region (rows past the actual length)
+  const int k = u - nu;
   const int pad_rows = is_hist ? a.G * (a.hb_bkt - hb) : (a.l.C_bkt - n);
-  float4 z[kMaxChunks];
+  if (k >= pad_rows) return;
+  float4 z[kChunks];
 #pragma unroll
-  for (int k = 0; k < kMaxChunks; ++k) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int k = wid; k < pad_rows; k += warps_per_grid_x) {
-    long long row;
-    if (is_hist) {
-      const int per = a.hb_bkt - hb;
-      const int g = k / per, i = hb + k % per;
-      row = static_cast<long long>(g) * a.l.R * a.hb_bkt + static_cast<long long>(r) * a.hb_bkt + i;
-    } else {
-      row = static_cast<long long>(r) * a.l.C_bkt + n + k;
-    }
-    assemble_row_st(a.o, is_hist, row, z, lane, a.D, a.d_true, RowStats{0.f, 0.f});
+  for (int q = 0; q < kChunks; ++q) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  long long row;
+  if (is_hist) {
+    const int per = a.hb_bkt - hb;
+    const int g = k / per, i = hb + k % per;
+    row = static_cast<long long>(g) * a.l.R * a.hb_bkt + static_cast<long long>(r) * a.hb_bkt + i;
+  } else {
+    row = static_cast<long long>(r) * a.l.C_bkt + n + k;
   }
+  assemble_row_st<kChunks>(a.o, is_hist, row, z, lane, a.D, a.d_true, RowStats{0.f, 0.f});
 }
 
 }  // namespace flame
