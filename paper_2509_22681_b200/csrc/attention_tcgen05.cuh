@@ -75,6 +75,31 @@ constexpr int kWGBytes = 7 * kTile;
 constexpr int kSmemBytes = 2 * kWGBytes + 1024 + 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef FLAME_ATTN_POLY_MASK
+#define FLAME_ATTN_POLY_MASK 0xA4  // pairs 2, 5, 7 of every 8 (3/8 of the exponentials)
+#endif
+constexpr unsigned kPolyMask = FLAME_ATTN_POLY_MASK;
+
+// exp2 of an fp32 pair on the FMA pipe (ptx::exp2_poly3, vectorised)
+__device__ __forceinline__ uint64_t exp2_poly3_x2(uint64_t x) {
+  float a, b;
+  f2::split(x, a, b);
+  x = f2::make(fmaxf(a, -126.0f), fmaxf(b, -126.0f));
+  const uint64_t M = f2::make(12582912.0f, 12582912.0f);
+  const uint64_t m1 = f2::make(-1.0f, -1.0f);
+  const uint64_t t = f2::add(x, M);      // round(x) in the low mantissa bits
+  const uint64_t r = f2::fma(M, m1, t);  // round(x), exact
+  const uint64_t f = f2::fma(r, m1, x);  // x - round(x) in [-0.5, 0.5], exact
+  uint64_t p = f2::fma(f2::make(0.05286737531423569f, 0.05286737531423569f), f,
+                       f2::make(0.24215202033519745f, 0.24215202033519745f));
+  p = f2::fma(p, f, f2::make(0.6935867667198181f, 0.6935867667198181f));
+  p = f2::fma(p, f, f2::make(0.9999627470970154f, 0.9999627470970154f));
+  float p0, p1, t0, t1;
+  f2::split(p, p0, p1);
+  f2::split(t, t0, t1);
+  return f2::make(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                  __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
 }  // namespace attn
 
 template <bool kHist>
@@ -85,7 +110,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
   const uint32_t raw_addr = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kWGBytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * 14);
 
   const int warp = threadIdx.x / 32;
   const int G = a.num_blocks;
@@ -93,19 +118,22 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
   const int bkt = kHist ? a.hb_bkt : a.c_bkt;
   const int n_tiles = (bkt + kRows - 1) / kRows;
 
-  // barriers of warpgroup i (13 slots each):
+  // barriers of warpgroup i (14 slots each):
   // 0 q_full (tx)  1 qs_free (128 WG + 1 control)  2,3 k_full  4,5 v_full
   // 6,7 kv_free (commit)  8 s_full (commit)  9 p_full (128)  10 o_full (commit)
   // 11 vself_full (tx: the candidates' own V rows for the job's end; for history
   //    rows a plain arrive that frees the output staging)  12 staging_ready (128)
-  auto B = [&](int i, int k) { return bars + i * 13 + k; };
+  // 13 s_free (128): the WG has S_c in registers, so S_{c+1} may overwrite the
+  //    S columns while the softmax of chunk c is still running
+  auto B = [&](int i, int k) { return bars + i * 14 + k; };
   if (threadIdx.x == 256) {
     ptx::tma_prefetch_desc(&tm_qkv);
     for (int i = 0; i < 2; ++i) {
-      for (int k = 0; k < 13; ++k) ptx::mbar_init(B(i, k), 1);
+      for (int k = 0; k < 14; ++k) ptx::mbar_init(B(i, k), 1);
       ptx::mbar_init(B(i, 1), 129);
       ptx::mbar_init(B(i, 9), 128);
       ptx::mbar_init(B(i, 12), 128);
+      ptx::mbar_init(B(i, 13), 128);
     }
     ptx::fence_barrier_init();
   }
@@ -251,13 +279,15 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
       s0_done = false;
       for (int c = 0; c < cur.nk; ++c, ++cc) {
         const int slot = resident ? c : (c & 1);
-        ptx::mbar_wait(B(i, 9), cc & 1);  // WG consumed S_c, stored P_c (and rescaled O)
-        ATTN_TRACE(2 + i, 14);
-        // S_{c+1} first: the warpgroup needs it next; PV_c is only needed at job end
+        // S_{c+1} as soon as the WG holds S_c in registers: it runs under the
+        // softmax of chunk c (PV_c is only needed before P_{c+1} is stored)
+        ptx::mbar_wait(B(i, 13), cc & 1);
         if (c + 1 < cur.nk) {
           issue_s(cur, c + 1);
           if (c + 1 == cur.nk - 1) prefetch_next_q();
         }
+        ptx::mbar_wait(B(i, 9), cc & 1);  // WG stored P_c (and rescaled O)
+        ATTN_TRACE(2 + i, 14);
         ptx::mbar_wait(B(i, 4 + slot), (kv_loads[slot] - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t aV = ptx::smem_u32(sV + slot * kTile);
@@ -391,6 +421,8 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
         for (int k = 0; k < kKeys / 32; ++k)
           ptx::tmem_ld_32x32b_x32(tS + k * 32, *reinterpret_cast<uint32_t(*)[32]>(s + k * 32));
         ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(B(i, 13));  // S columns free for S_{c+1}
         if (!full) {
 #pragma unroll
           for (int e = 0; e < kKeys; ++e)
@@ -412,31 +444,37 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
         const float alpha = (raise && m != -INFINITY) ? ptx::exp2_approx(m - m_new) : 1.f;
         m = m_new;
         const float m_use = (m == -INFINITY) ? 0.f : m;
-        // p = exp2(s*scale - m), packed to bf16 pairs in place (s[e/2] is dead)
-        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (full) {
-          // one pair in four on the FMA pipe (polynomial exp2): the MUFU is the
-          // softmax bottleneck with two warpgroups per SM
+        // p = exp2(s*scale - m) on fp32 pairs (FFMA2 / FADD2), packed to bf16 pairs in
+        // place (s[e/2] is dead).  kPolyMask selects the pairs (of every 8) whose exp2
+        // runs as a polynomial on the FMA pipe instead of the MUFU: once the loop is
+        // vectorised the MUFU, not the issue slots, is the limit.  Masked keys are
+        // -inf and give 0 (poly: 2^-126, below bf16 resolution of any sum).
+        const uint64_t sl2x2 = f2::make(sl2, sl2);
+        const uint64_t nm2 = f2::make(-m_use, -m_use);
+        uint64_t ps2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-          for (int e = 0; e < kKeys; e += 2) {
-            const float x0 = fmaf(__uint_as_float(s[e]), sl2, -m_use);
-            const float x1 = fmaf(__uint_as_float(s[e + 1]), sl2, -m_use);
-            const bool poly = ((e >> 1) & 3) == 3;
-            const float p0 = poly ? ptx::exp2_poly3(x0) : ptx::exp2_approx(x0);
-            const float p1 = poly ? ptx::exp2_poly3(x1) : ptx::exp2_approx(x1);
-            ps[(e >> 1) & 7] += p0 + p1;
-            s[e / 2] = pack_bf16x2(p0, p1);
+        for (int e = 0; e < kKeys; e += 2) {
+          const uint64_t x = f2::fma(f2::make(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), sl2x2, nm2);
+          uint64_t p;
+          if ((kPolyMask >> ((e >> 1) & 7)) & 1) {
+            p = exp2_poly3_x2(x);
+          } else {
+            float x0, x1;
+            f2::split(x, x0, x1);
+            p = f2::make(ptx::exp2_approx(x0), ptx::exp2_approx(x1));
           }
-        } else {
-#pragma unroll
-          for (int e = 0; e < kKeys; e += 2) {
-            const float p0 = ptx::exp2_approx(fmaf(__uint_as_float(s[e]), sl2, -m_use));
-            const float p1 = ptx::exp2_approx(fmaf(__uint_as_float(s[e + 1]), sl2, -m_use));
-            ps[(e >> 1) & 7] += p0 + p1;
-            s[e / 2] = pack_bf16x2(p0, p1);
-          }
+          ps2[(e >> 1) & 3] = f2::add(ps2[(e >> 1) & 3], p);
+          float p0, p1;
+          f2::split(p, p0, p1);
+          s[e / 2] = pack_bf16x2(p0, p1);
         }
-        const float psum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+        float psum;
+        {
+          float a0, a1, b0, b1;
+          f2::split(f2::add(f2::add(ps2[0], ps2[1]), f2::add(ps2[2], ps2[3])), a0, a1);
+          psum = a0 + a1;
+          (void)b0; (void)b1;
+        }
         l = l * alpha + psum;
         if (c > 0) {
           // PV(c-1) must be done before P is overwritten and O rescaled
