@@ -991,7 +991,7 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
     e->rs_h = static_cast<float*>(A(G * e->Rh * 4));
     e->rs_c = static_cast<float*>(A(e->Rc * 4));
     e->RS = static_cast<float*>(A(G * rows * 4));
-    e->stat_parts = gemm_row_parts(D, EPI_RESID | EPI_OUT_F32 | EPI_STATS);
+    e->stat_parts = gemm_row_parts(D, EPI_RESID | EPI_STATS);
     e->STATS = static_cast<float*>(A(G * rows * e->stat_parts * 2 * 4));
     const size_t n_parts = gemm_row_parts(F, EPI_BIAS | EPI_GELU | EPI_ROWDOT);
     if (c->tasks <= 4) e->partial = static_cast<float*>(A(e->Rc * n_parts * c->tasks * 4));

@@ -103,13 +103,16 @@ constexpr int kSmemBudget = 227 * 1024;
 // column sums u) of bf16-output variants are staged once per tile into a
 // per-warp smem slice and read back as broadcasts.  The smem ring gets whatever
 // the staging boxes leave (up to 6 stages).
+#ifndef FLAME_GEMM_OUT_BOXES
+#define FLAME_GEMM_OUT_BOXES 0
+#endif
 #ifndef FLAME_GEMM_HEAVY_WARPS
 #define FLAME_GEMM_HEAVY_WARPS 8
 #endif
 template <int BN, int EPI, int kCG>
 struct Cfg {
   static constexpr bool kHeavy = (EPI & (EPI_GELU | EPI_LNSTATS | EPI_STATS)) != 0;
-  static constexpr int kEpiWarps = kHeavy ? FLAME_GEMM_HEAVY_WARPS : 8;
+  static constexpr int kEpiWarps = (kHeavy && (EPI & EPI_OUT_F32) == 0) ? FLAME_GEMM_HEAVY_WARPS : 8;
   static constexpr int kEpiPerQuad = kEpiWarps / 4;
   static constexpr int kThreads = 128 + 32 * kEpiWarps;
   static constexpr bool kF32 = (EPI & EPI_OUT_F32) != 0;
@@ -120,9 +123,17 @@ struct Cfg {
   // STATS with an fp32 primary output, and the gated sum (hi + lo halves), also
   // stage a second bf16 box
   static constexpr bool kDual = ((EPI & EPI_STATS) != 0 && kF32) || kGated;
-  static constexpr int kOutBoxes = 1;
+  // staging slots per epilogue warp ([out box | bf16 side box]); with two, a
+  // chunk's staging does not wait for the previous chunk's TMA store to read smem.
+  // Measured at cfg3: pays for the GELU (FFN W1) epilogue (0.533 -> 0.497 ms),
+  // costs the others a smem ring stage (QKV 0.347 -> 0.394 ms), so by default
+  // (FLAME_GEMM_OUT_BOXES = 0) only the bf16 GELU variants get two.
+  static constexpr int kOutBoxes =
+      FLAME_GEMM_OUT_BOXES != 0 ? (FLAME_GEMM_OUT_BOXES == 2 && !kF32 ? 2 : 1)
+                                : ((EPI & EPI_GELU) != 0 && !kF32 && !kRowDot ? 2 : 1);
   static constexpr int kOutBoxBytes = kRowDot ? 0 : 32 * 32 * (kF32 ? 4 : 2);
-  static constexpr int kBoxBytes = kOutBoxes * kOutBoxBytes + (kDual ? 32 * 32 * 2 : 0);
+  static constexpr int kSlotBytes = kOutBoxBytes + (kDual ? 32 * 32 * 2 : 0);
+  static constexpr int kBoxBytes = kOutBoxes * kSlotBytes;
   // chunks of 32 columns per warp and the per-warp column-vector slices
   static constexpr int kChunks = BN / 32;
   static constexpr int kMyChunks = (kChunks + kEpiPerQuad - 1) / kEpiPerQuad;
@@ -329,7 +340,6 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     const int wq = warp & 3;    // TMEM lane quadrant this warp may access
     const int half = ew >> 2;   // which interleaved share of the 32-column chunks
     uint8_t* box = smem_box + ew * C::kBoxBytes;
-    uint8_t* box2 = box + C::kOutBoxBytes;  // bf16 side-output box (kDual)
     int box_i = 0;                           // alternating staging box (bf16 outputs)
     const bool epi_leader = ptx::elect_one();  // same lane issues stores and waits (bulk groups are per thread)
     // fp32 residual stream: this warp's valid chunks of all its tiles, in order;
@@ -399,8 +409,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         }
         __syncwarp();
       }
-      ptx::mbar_wait(&tmem_full[acc], acc_phase);
-      ptx::tc_fence_after();
+      // per-row operands (folded-LN rstd / mean) are loaded BEFORE the accumulator
+      // wait: their global-load latency then overlaps this tile's MMAs
       const int row0 = m_blk * gemm::BM + wq * 32;
       // rows past M are clipped by the TMA store; clamp their residual reads
       const int row = min(row0 + lane, ep.M - 1);
@@ -415,6 +425,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         const float2* pst = reinterpret_cast<const float2*>(ep.lnstats + g * ep.lnstats_gstride) +
                             static_cast<long long>(row) * ep.stats_parts;
         float s1 = 0.f, s2 = 0.f;
+#pragma unroll 4
         for (int k = 0; k < ep.stats_parts; ++k) {
           const float2 p = pst[k];
           s1 += p.x;
@@ -423,6 +434,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         ln_mean = s1 / ep.d_true;
         rs = rsqrtf(fmaxf(s2 / ep.d_true - ln_mean * ln_mean, 0.f) + 1e-5f);
       }
+      ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      ptx::tc_fence_after();
       // LN(x) W + b = rs * acc + (b - rs * mean * u)
       const uint64_t rs2 = f2::make(rs, rs);
       const uint64_t nm2 = f2::make(-rs * ln_mean, -rs * ln_mean);
@@ -572,7 +585,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         } else {
           if (epi_leader) ptx::tma_store_wait_read<C::kOutBoxes - 1>();  // this staging box free again
           __syncwarp();
-          uint8_t* ob = box + box_i * C::kOutBoxBytes;
+          uint8_t* ob = box + box_i * C::kSlotBytes;
+          uint8_t* box2 = ob + C::kOutBoxBytes;  // bf16 side-output box (kDual)
           if constexpr (C::kOutBoxes > 1) box_i ^= 1;
           if constexpr (C::kGated) {
             // split-bf16 expert operand: hi = bf16(sum), lo = bf16(sum - hi)
