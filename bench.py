@@ -54,6 +54,8 @@ WORKLOADS = {
              "Climber ranker: 4 blocks d=256, user seq 1024, 256 candidates/request"),
     "cfg3": (512, 64, 8, 1, 2048, 2, 2048, 512, 64,
              "production shape: 8 blocks d=512, user seq 2048, 512 candidates/request"),
+    "cfg4": (256, 64, 4, 1, 1024, 2, 1024, 2048, 256,
+             "DSO: Climber ranker d=256 4 blocks, user seq 1024, Zipf candidate counts 16-2048 per request"),
     "cfg5": (768, 64, 12, 1, 3072, 2, 8184, 1024, 8,
              "long-history stress: 12 blocks d=768, user seq 8184 (=12x682), 1024 candidates"),
 }
@@ -72,10 +74,20 @@ def zipf_sampler(num_items: int, exponent: float = 1.0):
     return lambda rng, n: np.searchsorted(cdf, rng.random(n)).astype(np.int64)
 
 
-def make_requests(n: int, H: int, C: int, seed: int):
+ZIPF_C = {"cfg4"}  # workloads with per-request candidate counts C = 16 + Zipf(1.0) rank over 2033
+
+
+def make_requests(n: int, H: int, C: int, seed: int, zipf_c: bool = False):
+    """n requests of (H history ids, C candidate ids), ids Zipf(1.0) over the item
+    universe (reference bench.py:130-144).  zipf_c: C_i = 16 + Zipf rank in
+    [0, 2033), so 16 <= C_i <= 2048 = C."""
     rng = np.random.default_rng(seed)
     sample = zipf_sampler(NUM_ITEMS)
-    return [(sample(rng, H), sample(rng, C)) for _ in range(n)]
+    if zipf_c:
+        counts = 16 + zipf_sampler(C - 16 + 1)(rng, n)
+    else:
+        counts = np.full(n, C)
+    return [(sample(rng, H), sample(rng, int(c))) for c in counts]
 
 
 def model_config(name: str):
@@ -181,7 +193,7 @@ def _oracle_worker(args):
 def cpu_reference_sample(name: str, n_requests: int, procs: int, seed: int) -> dict:
     """Time the oracle port on ``procs`` host processes (1 BLAS thread each)."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    reqs = make_requests(n_requests, WORKLOADS[name][6], WORKLOADS[name][7], seed)
+    reqs = make_requests(n_requests, WORKLOADS[name][6], WORKLOADS[name][7], seed, name in ZIPF_C)
     chunks = [(name, reqs[i::procs]) for i in range(procs) if reqs[i::procs]]
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
@@ -189,9 +201,8 @@ def cpu_reference_sample(name: str, n_requests: int, procs: int, seed: int) -> d
         res = pool.map(_oracle_worker, chunks)
     wall = time.perf_counter() - t0
     lat = sorted(x for _, l in res for x in l)
-    C = WORKLOADS[name][7]
     return {"wall_s": wall, "busy_s": max(r[0] for r in res), "requests": n_requests,
-            "cands": n_requests * C, "lat": lat, "procs": len(chunks)}
+            "cands": sum(len(c) for _, c in reqs), "lat": lat, "procs": len(chunks)}
 
 
 def nearest_rank(series, p):
@@ -202,7 +213,7 @@ def nearest_rank(series, p):
 
 
 # ------------------------------------------------------------------- main
-REF_REQS_PER_PROC = {"cfg1": 32, "cfg2": 2, "cfg3": 1, "cfg5": 1}
+REF_REQS_PER_PROC = {"cfg1": 32, "cfg2": 2, "cfg3": 1, "cfg4": 2, "cfg5": 1}
 
 
 def run_reference(args, dist) -> None:
@@ -216,13 +227,14 @@ def run_reference(args, dist) -> None:
     cpu = _cpu_name()
     for w in range(args.warmup):
         cpu_reference_sample(name, procs, procs, WORKLOAD_SEED + 7 + w)
-    step_s, lats = [], []
+    step_s, lats, cands = [], [], 0
     for k in range(args.steps):
         r = cpu_reference_sample(name, per * procs, procs, WORKLOAD_SEED + 100 + k)
         step_s.append(r["busy_s"])  # compute loop only: excludes worker spawn / imports
         lats += r["lat"]
+        cands += r["cands"]
     total = sum(step_s)
-    value = args.steps * per * procs * C / total
+    value = cands / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "candidates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -248,6 +260,58 @@ def _cpu_name() -> str:
     except OSError:
         pass
     return "unknown CPU"
+
+
+def roofline(prof_runs: list, name: str):
+    """Aggregate per-launch profiles ([[{name, ms, flops, bytes}]] of eager runs)
+    into per-kernel figures and the dominant kernel's roofline point."""
+    peaks, peak_src = load_peaks()
+    n_runs = len(prof_runs)
+    agg: dict = {}
+    for run in prof_runs:
+        for rec in run:
+            a = agg.setdefault(rec["name"], {"ms": 0.0, "n": 0, "flops": 0.0, "bytes": 0.0})
+            a["ms"] += rec["ms"]
+            a["n"] += 1
+            a["flops"] += rec["flops"]
+            a["bytes"] += rec["bytes"]
+    step_prof_ms = sum(a["ms"] for a in agg.values()) / n_runs
+    top = max(agg, key=lambda k: agg[k]["ms"])
+    t = agg[top]
+    avg_ms = t["ms"] / t["n"]
+    tensor = t["flops"] > 0
+    per_launch = (t["flops"] if tensor else t["bytes"]) / t["n"]
+    achieved = per_launch / (avg_ms / 1e3) / (1e12 if tensor else 1e9)
+    peak = peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]) if tensor \
+        else peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+    traffic = None
+    ncu = ROOT / "profiles" / "ncu_dram_per_launch.json"
+    if ncu.exists():
+        try:
+            traffic = json.loads(ncu.read_text()).get(name, {}).get(top)
+        except Exception:
+            traffic = None
+    kernels = {k: {"ms_per_step": round(v["ms"] / n_runs, 4),
+                   "share": round(v["ms"] / n_runs / step_prof_ms, 4),
+                   "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) if v["flops"] else None,
+                   "gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)}
+               for k, v in sorted(agg.items(), key=lambda kv: -kv[1]["ms"])}
+    return tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels
+
+
+def cpu_baseline_line(args, dist, name: str):
+    """The oracle port on this host's cores (rank 0, N = 1 only), bounded sample."""
+    if dist.world_size != 1 or args.no_cpu_baseline:
+        return None
+    cores = len(os.sched_getaffinity(0))
+    procs = max(1, min(cores, 32))
+    n_req = procs * 2 * REF_REQS_PER_PROC.get(name, 1)
+    r = cpu_reference_sample(name, n_req, procs, WORKLOAD_SEED + 99)
+    return {"value": r["cands"] / r["busy_s"], "unit": "candidates/s", "cores": r["procs"], "kind": "port",
+            "sample": f"{n_req} requests of {name} on {r['procs']} processes x 1 BLAS thread "
+                      f"({_cpu_name()}), numpy fp64 oracle port of reference "
+                      f"resolve_embeddings + model_forward; compute {r['busy_s']:.1f}s; "
+                      f"p99 {1000 * nearest_rank(r['lat'], 0.99):.0f} ms"}
 
 
 def run_ours(args, dist) -> None:
@@ -314,56 +378,144 @@ def run_ours(args, dist) -> None:
     d2h = R * C * tasks * 4
 
     # --------------------------------------------------- roofline (live)
-    peaks, peak_src = load_peaks()
-    prof_runs = 3
-    agg: dict = {}
-    for _ in range(prof_runs):
-        for rec in ex.profile(_lib.INPUT_IDS):
-            a = agg.setdefault(rec["name"], {"ms": 0.0, "n": 0, "flops": 0.0, "bytes": 0.0})
-            a["ms"] += rec["ms"]
-            a["n"] += 1
-            a["flops"] += rec["flops"]
-            a["bytes"] += rec["bytes"]
-    step_prof_ms = sum(a["ms"] for a in agg.values()) / prof_runs
-    top = max(agg, key=lambda k: agg[k]["ms"])
-    t = agg[top]
-    avg_ms = t["ms"] / t["n"]
-    tensor = t["flops"] > 0
-    per_launch = (t["flops"] if tensor else t["bytes"]) / t["n"]
-    achieved = per_launch / (avg_ms / 1e3) / (1e12 if tensor else 1e9)
-    peak = peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]) if tensor \
-        else peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
-    traffic = None
-    ncu = ROOT / "profiles" / "ncu_dram_per_launch.json"
-    if ncu.exists():
-        try:
-            traffic = json.loads(ncu.read_text()).get(name, {}).get(top)
-        except Exception:
-            traffic = None
-    kernels = {k: {"ms_per_step": round(v["ms"] / prof_runs, 4),
-                   "share": round(v["ms"] / prof_runs / step_prof_ms, 4),
-                   "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) if v["flops"] else None,
-                   "gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)}
-               for k, v in sorted(agg.items(), key=lambda kv: -kv[1]["ms"])}
+    prof = [ex.profile(_lib.INPUT_IDS) for _ in range(3)]
+    tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels = roofline(prof, name)
     from paper_2509_22681_b200.flops import algorithmic_flops
 
     step_flops = algorithmic_flops(cfg, H, C) * R
     step_tf = step_flops / (sum(step_ms) / args.steps / 1e3) / 1e12
 
     # ------------------------------------------------------ CPU baseline
-    cpu_baseline = None
-    if dist.world_size == 1 and not args.no_cpu_baseline:
-        cores = len(os.sched_getaffinity(0))
-        procs = max(1, min(cores, 32))
-        n_req = procs * 2 * REF_REQS_PER_PROC.get(name, 1)
-        r = cpu_reference_sample(name, n_req, procs, WORKLOAD_SEED + 99)
-        cpu_baseline = {"value": r["cands"] / r["busy_s"], "unit": "candidates/s", "cores": r["procs"],
-                        "kind": "port",
-                        "sample": f"{n_req} requests of {name} on {r['procs']} processes x 1 BLAS thread "
-                                  f"({_cpu_name()}), numpy fp64 oracle port of reference "
-                                  f"resolve_embeddings + model_forward; compute {r['busy_s']:.1f}s; "
-                                  f"p99 {1000 * nearest_rank(r['lat'], 0.99):.0f} ms"}
+    cpu_baseline = cpu_baseline_line(args, dist, name)
 
+    emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf, e2e_value, e2e_steps,
+              h2d, d2h, launches, tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels, clk,
+              cpu_baseline)
+
+
+def run_dso(args, dist) -> None:
+    """cfg4: non-uniform candidate counts through the DSO (BucketScheduler).
+
+    A step is one batch of R requests with C_i = 16 + Zipf rank (16..2048),
+    H = 1024.  The scheduler buckets them by (history, candidate) powers of
+    two into groups of up to slots_for(c_bkt) requests, one CUDA-graph replay
+    per group, each bucket's executors on their own streams.
+    * value: every group pre-staged in its own executor (ids resident in HBM);
+      a step replays all groups concurrently on their streams (fork/join
+      events on the step stream); real candidates / device time.
+    * e2e:   BucketScheduler.score(ids=True) from numpy ids to numpy scores per
+      step (pinned staging, async submit/collect across a ring of executors
+      per bucket); p99 = per-request time from the call to its group's
+      collection, nearest rank over all steps, max over ranks.
+    """
+    import torch
+
+    import paper_2509_22681_b200 as fb
+    from paper_2509_22681_b200 import _lib
+    from paper_2509_22681_b200.flops import algorithmic_flops
+    from paper_2509_22681_b200.orchestrator import BucketScheduler
+    from paper_2509_22681_b200.pda import build_item_table
+
+    name = args.workload
+    d, dh, nb, L, f, tasks, H, C, R_default, desc = WORKLOADS[name]
+    R = args.requests or R_default
+    dev = torch.device("cuda", dist.local_rank)
+    torch.cuda.set_device(dev)
+    cfg = model_config(name)
+    eng = fb.FlameEngine(fb.init_params(cfg), cfg, precision="bf16", device=dist.local_rank)
+    eng.set_table(build_item_table(NUM_ITEMS, d, STORE_SEED), dtype="fp32")
+    reqs = make_requests(R, H, C, WORKLOAD_SEED + dist.rank, zipf_c=True)
+    counts = [len(c) for _, c in reqs]
+    n_cand = sum(counts)
+    sched = BucketScheduler(eng, with_ids=True)
+    plan = sched.plan([(len(h), len(c)) for h, c in reqs])
+    bucket_rows = sum(len(idx) * cb for (hb, cb), idx in plan)  # unused slots are skipped on the device
+    # device-timed: one dedicated executor per group, ids staged once
+    groups = []
+    for (hb, cb), idx in plan:
+        ex = eng.executor(sched.slots_for(cb), hb, cb, with_ids=True)
+        ex.stage_ids([reqs[i] for i in idx])
+        ex.run(_lib.INPUT_IDS, graph=True)
+        groups.append(ex)
+    torch.cuda.synchronize()
+    launches = sum(ex.launch_count() for ex in groups)
+    main = torch.cuda.Stream(device=dev)
+
+    def step(ev_start, ev_end):
+        with torch.cuda.stream(main):
+            ev_start.record(main)
+        joins = []
+        for ex in groups:
+            ex.stream.wait_event(ev_start)
+            ex.run(_lib.INPUT_IDS, graph=True)
+            j = torch.cuda.Event()
+            j.record(ex.stream)
+            joins.append(j)
+        for j in joins:
+            main.wait_event(j)
+        with torch.cuda.stream(main):
+            ev_end.record(main)
+
+    for _ in range(args.warmup):
+        step(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in evs:
+        step(a, b)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = dist.max(sum(step_ms))
+    value = n_cand * args.steps * dist.world_size / (total_ms / 1e3)
+
+    # e2e through the scheduler (async submit / collect over the executor rings)
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        sched.score(reqs, ids=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    lats = []
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sched.score(reqs, ids=True)
+        lats += sched.last_latencies
+    e2e_s = dist.max(time.perf_counter() - t0)
+    e2e_value = n_cand * e2e_steps * dist.world_size / e2e_s
+    p99 = dist.max(1000 * nearest_rank(lats, 0.99))
+    h2d = sum(len(h) + len(c) for h, c in reqs) * 8 + 3 * 4 * len(plan)
+    d2h = n_cand * tasks * 4
+
+    prof = [[rec for ex in groups for rec in ex.profile(_lib.INPUT_IDS)] for _ in range(2)]
+    tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels = roofline(prof, name)
+    step_flops = sum(algorithmic_flops(cfg, H, c) for c in counts)
+    step_tf = step_flops / (sum(step_ms) / args.steps / 1e3) / 1e12
+    cpu_baseline = cpu_baseline_line(args, dist, name)
+    hist = {}
+    for (hb, cb), idx in plan:
+        hist[str(cb)] = hist.get(str(cb), 0) + len(idx)
+    step_p99 = dist.max(nearest_rank(step_ms, 0.99))
+    emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf,
+              e2e_value, e2e_steps, h2d, d2h, launches, tensor, top, achieved, peak, traffic, peak_src, per_launch,
+              avg_ms, kernels, clk, cpu_baseline,
+              extra_config={"candidates_per_request": "16 + Zipf(1.0) rank over 2033 (16..2048)",
+                            "candidates_per_step_per_gpu": n_cand, "groups_per_step": len(plan),
+                            "step_p99_ms": step_p99,
+                            "requests_per_bucket": hist, "padding_efficiency": round(n_cand / bucket_rows, 4),
+                            "dso": "BucketScheduler: pow2 (history, candidate) buckets, one graph replay per group, "
+                                   "one stream per executor, groups concurrent"},
+              e2e_path="BucketScheduler.score(ids=True): numpy ids -> pinned -> H2D -> graph per group -> D2H -> numpy",
+              latency_note="p99_ms: per-request latency on the e2e path (call -> its group's scores on the host), "
+                           "nearest rank over all e2e steps, max over ranks; device step p99 in step_p99_ms")
+
+
+def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf, e2e_value, e2e_steps,
+              h2d, d2h, launches, tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels, clk,
+              cpu_baseline, extra_config=None, e2e_path=None, latency_note=None):
     if dist.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": dist.world_size,
@@ -378,12 +530,12 @@ def run_ours(args, dist) -> None:
                        "l2": "per-step working set (activations, several GB) >> 126 MB L2; no flush",
                        "input": "item ids resident in HBM; PDA gather from the fp32 HBM item table"},
             "p99_ms": p99,
-            "latency_note": "a request completes when its step's graph replay completes; "
-                            "p99 over steps (nearest rank), max over ranks",
+            "latency_note": latency_note or ("a request completes when its step's graph replay completes; "
+                                             "p99 over steps (nearest rank), max over ranks"),
             "step_tflops": round(step_tf, 1),
             "e2e": {"value": e2e_value, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                    "path": "DeviceExecutor.score_ids: numpy ids -> pinned -> H2D -> graph -> D2H -> numpy"},
+                    "path": e2e_path or "DeviceExecutor.score_ids: numpy ids -> pinned -> H2D -> graph -> D2H -> numpy"},
             "gpu_launches": launches * args.steps,
             "launches_per_step": launches,
             "roofline": {"bound": "tensor" if tensor else "hbm", "kernel": top,
@@ -396,6 +548,8 @@ def run_ours(args, dist) -> None:
             "clocks": clk,
             "cpu_baseline": cpu_baseline,
         }
+        if extra_config:
+            line["config"].update(extra_config)
         print(json.dumps(line), flush=True)
 
 
@@ -417,6 +571,8 @@ def main() -> None:
     try:
         if args.impl == "reference":
             run_reference(args, dist)
+        elif args.workload in ZIPF_C:
+            run_dso(args, dist)
         else:
             run_ours(args, dist)
     finally:

@@ -77,6 +77,9 @@ typedef struct FlameIO {
   long long* unique_ids;      /* [2R][cap] per list: np.unique values (lists: R history, then R candidate) */
   long long* inverse;         /* [2R][cap] per list: np.unique inverse */
   int* n_unique;              /* [2R] */
+  const int* active;          /* [1] slots 0..active-1 are in use this run (NULL: all R).  Read on the
+                                 device, so one captured graph serves any batch size <= R: the
+                                 kernels skip the rows, units and lists of the unused slots */
 } FlameIO;
 
 int flame_create(const FlameModelDesc* cfg, const double* weights_fp64, long long n_values,

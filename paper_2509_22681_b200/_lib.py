@@ -37,7 +37,7 @@ class FlameModelDesc(ctypes.Structure):
 class FlameIO(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "hist_emb", "cand_emb", "hist_ids", "cand_ids", "hist_len", "cand_len", "out_offset",
-        "scores", "unique_ids", "inverse", "n_unique")]
+        "scores", "unique_ids", "inverse", "n_unique", "active")]
 
 
 _lib = None

@@ -48,6 +48,7 @@ struct AttnArgs {
   const int* cand_len;       // [R] actual candidate count C_r
   const float* scale_log2;   // [G] log2(e) / (tau_g * sqrt(head_dim))
   int store_tma;             // 1: 128-row output tiles never cross a request (bkt % 128 == 0)
+  const int* active;         // [1] requests in use (null: all R); units of unused slots are skipped
 };
 
 // Debug-only event trace of CTA 0 (set through flame_debug_attn_trace): slot 0/1 =
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
 
   const int warp = threadIdx.x / 32;
   const int G = a.num_blocks;
-  const int n_units = a.R * G * a.nh;
+  const int R_eff = a.active != nullptr ? min(a.R, __ldg(a.active)) : a.R;
+  const int n_units = R_eff * G * a.nh;
   const int bkt = kHist ? a.hb_bkt : a.c_bkt;
   const int n_tiles = (bkt + kRows - 1) / kRows;
 

@@ -465,6 +465,11 @@ struct Pipe {
     ep.lnstats = ln.lnstats; ep.lnstats_gstride = ln.lnstats_gstride; ep.stats_parts = ln.stats_parts;
     ep.d_true = ln.d_true; ep.colsum = ln.colsum; ep.colsum_gstride = ln.colsum_gstride;
     ep.resid_b = resid_b; ep.gate_w = gate_w; ep.gate_b = gate_b;
+    if (e->io.active != nullptr && e->R > 0 && (M == e->Rh || M == e->Rc) && M % e->R == 0) {
+      // a slot-major row range (all history rows or all candidate rows): skip unused slots
+      ep.m_active = e->io.active;
+      ep.rows_per_slot = static_cast<int>(M / e->R);
+    }
     rs_ptr = nullptr; rs_g = 0; dot_w = nullptr; dot_n = 0; ln = GemmEpilogue{}; resid_b = nullptr;
     gate_w = nullptr; gate_b = nullptr;
     if (M <= 0) return 0;
@@ -538,6 +543,7 @@ struct Pipe {
       a.out_ld = c->DA; a.out_gstride = e->rows * static_cast<long long>(c->DA);
       a.DA = c->DA; a.R = e->R; a.hb_bkt = e->hb_bkt; a.c_bkt = e->c_bkt; a.num_blocks = c->G;
       a.hist_len = e->io.hist_len; a.cand_len = e->io.cand_len; a.scale_log2 = c->scale_log2;
+      a.active = e->io.active;
       CUtensorMap tm;
       if (!make_tmap_bf16_3d(&tm, e->QKV, 3ULL * c->DA, e->rows, c->G, 3ULL * c->DA * 2,
                              e->rows * 3ULL * c->DA * 2, 64, 128))
@@ -607,7 +613,7 @@ struct Pipe {
     l.unique = e->io.unique_ids ? e->io.unique_ids : e->unique_ws;
     l.inverse = e->io.inverse ? e->io.inverse : e->inverse_ws;
     l.n_unique = e->io.n_unique ? e->io.n_unique : e->nuniq_ws;
-    l.spos = e->spos; l.ustart = e->ustart; l.cap = e->cap;
+    l.spos = e->spos; l.ustart = e->ustart; l.cap = e->cap; l.active = e->io.active;
     int P = 1;
     while (P < e->cap) P <<= 1;
     const int smem = P * 16;
@@ -617,14 +623,16 @@ struct Pipe {
       smem_set = smem;
     }
     mark("pda_dedup", 0.0, static_cast<double>(e->R) * (e->H_bkt + e->c_bkt) * (8.0 + 8.0 + 8.0 + 8.0));
-    pda_dedup<<<2 * e->R, kPdaThreads, smem, s>>>(l);
+    const int dthreads = P / 2 < 64 ? 64 : (P / 2 > kPdaThreads ? kPdaThreads : P / 2);
+    pda_dedup<<<2 * e->R, dthreads, smem, s>>>(l);
     if (int rc = check()) return rc;
     {
       PdaGatherArgs g{};
       g.l = l; g.table = c->table; g.num_items = c->num_items; g.D = c->D; g.d_true = c->d; g.G = c->G;
       g.hb_bkt = e->hb_bkt; g.o = assemble_out();
-      // one warp per unique id, plus one per padding row (together <= 2 x capacity)
-      dim3 grid(static_cast<unsigned>((2 * e->cap + 7) / 8), 2 * e->R);
+      // one warp per unique id, plus one per padding row (together <= the list
+      // capacity); up to 4 of them per warp
+      dim3 grid(static_cast<unsigned>((e->cap + 31) / 32), 2 * e->R);
       // rows out + table rows read (upper bound: one per position); candidates also get fp32
       const double tab = c->table_dtype == FLAME_TABLE_BF16 ? 2.0 : 4.0;
       mark("pda_gather", 0.0, static_cast<double>(e->R) * c->D *

@@ -68,6 +68,10 @@ struct GemmEpilogue {
   // reaches HBM, as the split-bf16 [hi | hi | lo] expert operand ([M][3N] bf16)
   const float* gate_w;    // [G][N]
   const float* gate_b;    // [G][N]
+  // device-side active row count (DSO executors): rows >= *m_active * rows_per_slot
+  // are unused slots and their tiles are skipped (null: all M rows)
+  const int* m_active;
+  int rows_per_slot;
   int M, N;               // logical bounds of this problem
   int g_inner;            // tile order: 1 = group index fastest (operand / residual shared by all groups)
 };
@@ -165,7 +169,7 @@ template <int BN, int EPI, int kCG>
 __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
-                      const __grid_constant__ CUtensorMap tmR, int num_k_blocks, int m_tiles, int n_tiles, int groups, int a_shared, GemmEpilogue ep) {
+                      const __grid_constant__ CUtensorMap tmR, int num_k_blocks, int m_tiles_max, int n_tiles, int groups, int a_shared, GemmEpilogue ep) {
   using C = gemm::Cfg<BN, EPI, kCG>;
   constexpr int kEpiWarps = C::kEpiWarps;
   constexpr int kEpiPerQuad = kEpiWarps / 4;
@@ -193,6 +197,11 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   // halves of a 256-row tile; the even CTA issues cta_group::2 MMAs for both
   constexpr int ncl = kCG;
   const int crank = kCG == 2 ? static_cast<int>(ptx::cluster_ctarank()) : 0;
+  int m_tiles = m_tiles_max;
+  if (ep.m_active != nullptr) {
+    const int rows = __ldg(ep.m_active) * ep.rows_per_slot;
+    m_tiles = max(1, min(m_tiles_max, (rows + gemm::BM - 1) / gemm::BM));
+  }
   const int m_pairs = (m_tiles + ncl - 1) / ncl;
   const int cid = blockIdx.x / ncl;
   const int nclusters = gridDim.x / ncl;

@@ -37,6 +37,7 @@ struct PdaLists {
   int* spos;           // [2R][cap] positions in sorted order
   int* ustart;         // [2R][cap] run start (index into spos) of each unique id
   int cap;             // max(H_bkt, C_bkt)
+  const int* active;   // [1] requests in use (null: all R); lists of unused slots are skipped
 };
 
 __device__ __forceinline__ bool pair_less(long long ka, int pa, long long kb, int pb) {
@@ -48,6 +49,10 @@ __global__ void __launch_bounds__(kPdaThreads) pda_dedup(PdaLists a) {
   const int list = blockIdx.x;
   const bool is_hist = list < a.R;
   const int r = is_hist ? list : list - a.R;
+  if (a.active != nullptr && r >= __ldg(a.active)) {
+    if (threadIdx.x == 0) a.n_unique[list] = 0;
+    return;
+  }
   const int n = is_hist ? a.hist_len[r] : a.cand_len[r];
   const long long* ids = is_hist ? a.hist_ids + static_cast<long long>(r) * a.H_bkt
                                  : a.cand_ids + static_cast<long long>(r) * a.C_bkt;
@@ -62,20 +67,20 @@ __global__ void __launch_bounds__(kPdaThreads) pda_dedup(PdaLists a) {
     pos[i] = i;
   }
   __syncthreads();
-  // bitonic sort, ascending by (id, position)
+  // bitonic sort, ascending by (id, position): one compare-exchange pair per
+  // thread per pass (P / 2 pairs; the block is sized to the bucket's P / 2)
   for (int k = 2; k <= P; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const long long ki = key[i], kj = key[ixj];
-          const int pi = pos[i], pj = pos[ixj];
-          const bool gt = pair_less(kj, pj, ki, pi);
-          if (gt == up) {
-            key[i] = kj; key[ixj] = ki;
-            pos[i] = pj; pos[ixj] = pi;
-          }
+      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+        const int i = (t / j) * 2 * j + (t % j);
+        const int ixj = i + j;
+        const bool up = (i & k) == 0;
+        const long long ki = key[i], kj = key[ixj];
+        const int pi = pos[i], pj = pos[ixj];
+        const bool gt = pair_less(kj, pj, ki, pi);
+        if (gt == up) {
+          key[i] = kj; key[ixj] = ki;
+          pos[i] = pj; pos[ixj] = pi;
         }
       }
       __syncthreads();
@@ -182,11 +187,15 @@ __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
   const int list = blockIdx.y;
   const bool is_hist = list < a.l.R;
   const int r = is_hist ? list : list - a.l.R;
+  if (a.l.active != nullptr && r >= __ldg(a.l.active)) return;  // unused slot: its rows are never read
   const int n = is_hist ? a.l.hist_len[r] : a.l.cand_len[r];
   const int nu = a.l.n_unique[list];
   const int lane = threadIdx.x % 32;
-  const int u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int hb = is_hist ? n / a.G : 0;
+  const int pad_rows = is_hist ? a.G * (a.hb_bkt - hb) : (a.l.C_bkt - n);
+  const int work = nu + pad_rows;  // <= list capacity
+  const int stride = gridDim.x * (blockDim.x / 32);
+  for (int u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; u < work; u += stride) {
   auto row_of = [&](int p) -> long long {  // destination row of list position p
     if (is_hist) {
       const int g = p / hb, i = p % hb;
@@ -218,12 +227,10 @@ __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
         assemble_row_st<kChunks>(a.o, is_hist, row_of(__shfl_sync(0xffffffffu, pos, j)), v, lane, a.D,
                                  a.d_true, st);
     }
-    return;
+    continue;
   }
   // zero the padding rows of this list's region (rows past the actual length)
   const int k = u - nu;
-  const int pad_rows = is_hist ? a.G * (a.hb_bkt - hb) : (a.l.C_bkt - n);
-  if (k >= pad_rows) return;
   float4 z[kChunks];
 #pragma unroll
   for (int q = 0; q < kChunks; ++q) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -236,6 +243,7 @@ __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
     row = static_cast<long long>(r) * a.l.C_bkt + n + k;
   }
   assemble_row_st<kChunks>(a.o, is_hist, row, z, lane, a.D, a.d_true, RowStats{0.f, 0.f});
+  }
 }
 
 }  // namespace flame

@@ -152,11 +152,13 @@ class DeviceExecutor:
 
         self.hist_emb = dalloc((R, self.H_bkt, d), torch.float32)
         self.cand_emb = dalloc((R, c_bkt, d), torch.float32)
-        self.hist_len = dalloc((R,), torch.int32)
-        self.cand_len = dalloc((R,), torch.int32)
-        self.out_offset = dalloc((R,), torch.int32)
+        # per-slot metadata in one block (one H2D per batch): hist_len, cand_len,
+        # out_offset, and [3][0] = active slot count
+        self.meta = dalloc((4, R), torch.int32)
+        self.hist_len, self.cand_len, self.out_offset = self.meta[0], self.meta[1], self.meta[2]
+        self.active = self.meta[3, :1]
         self.scores = dalloc((R * c_bkt, tasks), torch.float32)
-        self.h_meta = halloc((3, R), torch.int32)
+        self.h_meta = halloc((4, R), torch.int32)
         self.h_scores = halloc((R * c_bkt, tasks), torch.float32)
         self.h_hist = halloc((R, self.H_bkt, d), torch.float32)
         self.h_cand = halloc((R, c_bkt, d), torch.float32)
@@ -170,6 +172,8 @@ class DeviceExecutor:
             self.h_hist_ids = halloc((R, self.H_bkt), torch.int64)
             self.h_cand_ids = halloc((R, c_bkt), torch.int64)
         self.stream = torch.cuda.Stream(device=dev)
+        self._done = torch.cuda.Event()
+        self._pending = None
         self._dummy = torch.zeros(16, dtype=torch.float32, device=dev)
 
         def ptr(t):
@@ -184,7 +188,8 @@ class DeviceExecutor:
             ptr(self.hist_len), ptr(self.cand_len), ptr(self.out_offset), ptr(self.scores),
             ptr(self.unique) if with_ids else None,
             ptr(self.inverse) if with_ids else None,
-            ptr(self.n_unique) if with_ids else None)
+            ptr(self.n_unique) if with_ids else None,
+            ptr(self.active))
         ex = ctypes.c_void_p()
         with torch.cuda.device(dev):
             _lib.check(engine.lib.flame_exec_create(engine.handle, R, hb_bkt, c_bkt, ctypes.byref(io),
@@ -207,6 +212,7 @@ class DeviceExecutor:
         offs = np.zeros(R, dtype=np.int64)
         offs[1:n] = np.cumsum(np.asarray(cand_lens, dtype=np.int64))[:-1] if n > 1 else 0
         meta[2, :n] = offs[:n]
+        meta[3, 0] = n  # slots n..R-1 are skipped by the kernels (one graph serves any n <= R)
         self.n_real = int(np.sum(cand_lens))
         return n
 
@@ -256,9 +262,7 @@ class DeviceExecutor:
             self._upload_meta()
 
     def _upload_meta(self) -> None:
-        self.hist_len.copy_(self.h_meta[0], non_blocking=True)
-        self.cand_len.copy_(self.h_meta[1], non_blocking=True)
-        self.out_offset.copy_(self.h_meta[2], non_blocking=True)
+        self.meta.copy_(self.h_meta, non_blocking=True)
 
     # ------------------------------------------------------------- running
     def run(self, mode: int = _lib.INPUT_EMBEDDINGS, graph: bool = True) -> None:
@@ -283,18 +287,48 @@ class DeviceExecutor:
     def score(self, requests, graph: bool = True) -> list[np.ndarray]:
         """Score a batch of (history, candidates) embedding requests."""
         with self.lock:
-            self.stage_embeddings(requests)
-            self.run(_lib.INPUT_EMBEDDINGS, graph)
-            flat = self.fetch_scores()
-        return _split_rows(flat, [c.shape[0] for _, c in requests])
+            self.submit(requests, ids=False, graph=graph)
+            return self.collect()
 
     def score_ids(self, requests, graph: bool = True) -> list[np.ndarray]:
         """Score a batch of (history ids, candidate ids) requests via the PDA path."""
         with self.lock:
+            self.submit(requests, ids=True, graph=graph)
+            return self.collect()
+
+    # ------------------------------------------------- asynchronous use (DSO)
+    def submit(self, requests, ids: bool, graph: bool = True) -> None:
+        """Stage a batch, replay the forward pass and queue the score D2H, all on
+        this executor's stream, without waiting.  ``collect`` returns the scores.
+        The pinned staging buffers are reused, so a second ``submit`` must come
+        after the first ``collect`` (the DSO keeps a ring of executors per bucket)."""
+        if self._pending is not None:
+            raise RuntimeError("executor has an uncollected batch")
+        if ids:
             self.stage_ids(requests)
-            self.run(_lib.INPUT_IDS, graph)
-            flat = self.fetch_scores()
-        return _split_rows(flat, [len(c) for _, c in requests])
+        else:
+            self.stage_embeddings(requests)
+        self.run(_lib.INPUT_IDS if ids else _lib.INPUT_EMBEDDINGS, graph)
+        n = self.n_real
+        with torch.cuda.stream(self.stream):
+            self.h_scores[:n].copy_(self.scores[:n], non_blocking=True)
+            self._done.record(self.stream)
+        self._pending = [len(c) for _, c in requests]
+
+    @property
+    def pending(self) -> bool:
+        return self._pending is not None
+
+    def ready(self) -> bool:
+        return self._pending is not None and self._done.query()
+
+    def collect(self) -> list[np.ndarray]:
+        if self._pending is None:
+            raise RuntimeError("nothing submitted")
+        self._done.synchronize()
+        counts, self._pending = self._pending, None
+        flat = self.h_scores[: self.n_real].numpy().astype(np.float64)
+        return _split_rows(flat, counts)
 
     def profile(self, mode: int = _lib.INPUT_EMBEDDINGS, max_launches: int = 256) -> list[dict]:
         """One eager run with per-launch CUDA events on this executor's stream:

@@ -99,3 +99,29 @@ def test_bucket_scheduler_zipf_candidates(gpu):
     for (h, c), s in zip(reqs[:10], got[:10]):
         np.testing.assert_array_equal(s, fb.model_forward(h, c, params, cfg))
     assert all(s.shape == (len(c), 2) for (_, c), s in zip(reqs, got))
+
+
+def test_bucket_scheduler_ring_and_ids(gpu):
+    """Many groups per bucket (small target_rows) wrap each bucket's executor ring:
+    async submit/collect must still return every request's exact scores; the id
+    path (device PDA) must equal embedding-path scoring of the same rows."""
+    from paper_2509_22681_b200.pda import build_item_table
+
+    cfg = fb.ModelConfig(64, 16, 4, 1, 256, 2, 256, 256, seed=3)
+    params = fb.init_params(cfg)
+    eng = fb.FlameEngine(params, cfg, "bf16")
+    table = build_item_table(500, 64)
+    eng.set_table(table, dtype="fp32")
+    sched = BucketScheduler(eng, target_rows=64, with_ids=True, executors_per_bucket=2)
+    rng = np.random.default_rng(7)
+    counts = rng.integers(1, 200, 30)
+    reqs = [(rng.integers(0, 500, 256), rng.integers(0, 500, int(c))) for c in counts]
+    plan = sched.plan([(256, int(c)) for c in counts])
+    assert max(sum(1 for k, _ in plan if k == key) for key, _ in plan) > 2  # ring wraps
+    got = sched.score(reqs, ids=True)
+    assert len(sched.last_latencies) == len(reqs) and min(sched.last_latencies) > 0
+    emb = BucketScheduler(eng, target_rows=64)
+    want = emb.score([(table[h], table[c]) for h, c in reqs])
+    for g, w, c in zip(got, want, counts):
+        assert g.shape == (int(c), 2)
+        np.testing.assert_array_equal(g, w)

@@ -93,3 +93,13 @@ def test_sharding_gloo_world2():
     assert set(a[0]).isdisjoint(b[0]) and sorted(a[0] + b[0]) == list(range(6))
     assert a[1] == b[1] == 2.0  # max over ranks
     assert a[2] == b[2] == 212.0  # every candidate scored exactly once
+
+
+def test_candidate_buckets():
+    from paper_2509_22681_b200.orchestrator import cand_bucket
+
+    assert [cand_bucket(c) for c in (1, 16, 17, 100, 129, 257, 300, 384, 385, 600, 768, 769, 1100, 1536, 1537)] == \
+        [16, 16, 32, 128, 256, 384, 384, 384, 512, 768, 768, 1024, 1536, 1536, 2048]
+    for c in range(1, 2049):
+        b = cand_bucket(c)
+        assert b >= c and (b < 128 or b % 128 == 0)
