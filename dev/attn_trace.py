@@ -18,7 +18,7 @@ lib.flame_debug_attn_trace(ctypes.c_void_p(buf.data_ptr()))
 ex.run(_lib.INPUT_IDS, graph=False); ex.stream.synchronize()
 lib.flame_debug_attn_trace(None)
 t = buf.cpu().numpy().astype(np.uint64).reshape(4, 4096)
-names = {1: "job", 2: "q_ok", 3: "s_ok", 4: "p_arr", 5: "o_ok", 11: "C:job", 12: "C:q_ok", 13: "C:S", 14: "C:p_ok", 15: "C:PV"}
+names = {1: "job", 2: "q_ok", 3: "s_ok", 4: "p_arr", 5: "o_ok", 6: "s_ld", 7: "max", 8: "exp", 9: "pv_ok", 11: "C:job", 12: "C:q_ok", 13: "C:S", 14: "C:p_ok", 15: "C:PV"}
 t0 = min(int(x >> 8) for row in t for x in row if x)
 for slot in range(4):
     ev = [(int(x >> 8) - t0, int(x & 0xff)) for x in t[slot] if x]
