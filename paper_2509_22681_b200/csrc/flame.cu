@@ -1137,6 +1137,15 @@ void* flame_exec_workspace(FlameExec* e, const char* name) {
 
 // Debug-only (not part of the public header): route the attention kernel's CTA-0
 // event trace into a caller-owned device buffer of 4 x 4096 uint64 (NULL = off).
+extern "C" int flame_debug_gemm_trace(void* dev_buf, int which) {
+  flame::g_gemm_trace_buf = static_cast<unsigned long long*>(dev_buf);
+  flame::g_gemm_trace_which = which;
+  flame::g_gemm_trace_count = 0;
+  unsigned long long* p = nullptr;
+  CUDA_TRY(cudaMemcpyToSymbol(flame::g_gemm_trace, &p, sizeof(p)));
+  return 0;
+}
+
 extern "C" int flame_debug_attn_trace(void* dev_buf) {
   unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
   CUDA_TRY(cudaMemcpyToSymbol(flame::g_attn_trace, &p, sizeof(p)));

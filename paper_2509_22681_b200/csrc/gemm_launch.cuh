@@ -160,8 +160,18 @@ static int gemm_row_parts(int N, int epi) {
   return ((N + bn - 1) / bn) * (heavy ? FLAME_GEMM_HEAVY_WARPS / 4 : 2);
 }
 
+// debug: trace (g_gemm_trace) only the which-th GEMM launched after flame_debug_gemm_trace
+static unsigned long long* g_gemm_trace_buf = nullptr;
+static int g_gemm_trace_which = -1, g_gemm_trace_count = 0;
+
 static cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t s, int num_sms) {
   if (p.K % gemm::BK != 0 || p.M < 1 || p.N < 1 || p.G < 1) return cudaErrorInvalidValue;
+  if (g_gemm_trace_buf != nullptr) {
+    unsigned long long* v = g_gemm_trace_count++ == g_gemm_trace_which ? g_gemm_trace_buf : nullptr;
+    cudaError_t e = cudaMemcpyToSymbolAsync(g_gemm_trace, &v, sizeof(v), 0, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    cudaStreamSynchronize(s);  // the host copy source is a local
+  }
   constexpr int kGatedW2 = EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_GATED;
   if (p.epi & EPI_GATED) {
     if (p.epi != kGatedW2 || p.N % 32 != 0) return cudaErrorInvalidValue;

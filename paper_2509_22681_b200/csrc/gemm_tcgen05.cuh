@@ -93,6 +93,18 @@ enum : int {
   EPI_GATED = 512,
 };
 
+// Debug-only event trace of CTA 0 (flame_debug_gemm_trace): slot 0 = MMA issuer,
+// slot 1 = epilogue warp 0, slot 2 = epilogue warp 4, slot 3 = producer;
+// entry = clock64 << 8 | code.  One writer per slot, no atomics.
+__device__ unsigned long long* g_gemm_trace = nullptr;
+#define GEMM_TRACE(slot, code)                                                                  \
+  do {                                                                                          \
+    if (g_gemm_trace != nullptr && blockIdx.x == 0 && lane == 0) {                              \
+      if (gtrace_k < 4096) g_gemm_trace[(slot) * 4096 + gtrace_k] = (clock64() << 8) | (code);  \
+      ++gtrace_k;                                                                               \
+    }                                                                                           \
+  } while (0)
+
 namespace gemm {
 
 constexpr int BM = 128;
@@ -261,6 +273,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     const bool leader = ptx::elect_one();
     int stage = 0;
     uint32_t phase = 0;
+    unsigned gtrace_k = 0;
     for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int g, mp, n_blk;
       decode(tile, g, mp, n_blk);
@@ -269,6 +282,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       const int ga = a_shared ? 0 : g;
       for (int kb = 0; kb < num_k_blocks; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
+        GEMM_TRACE(3, 7);
 #ifdef FLAME_DBG_GEMM_NO_TMA
         if (leader) ptx::mbar_arrive(&full[stage]);
         if (false) {
@@ -311,12 +325,15 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    unsigned gtrace_k = 0;
     for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       ptx::mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+      GEMM_TRACE(0, 1);
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < num_k_blocks; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
+        if (kb == 0) GEMM_TRACE(0, 2);
         ptx::tc_fence_after();
         const uint32_t a_addr = ptx::smem_u32(smem_a + stage * C::kABytes);
         const uint32_t b_addr = ptx::smem_u32(smem_b + stage * C::kBBytes);
@@ -339,6 +356,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         else ptx::mma_commit_cg2_mc(&tmem_full[acc], 0x3);
       }
       __syncwarp();
+      GEMM_TRACE(0, 3);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
@@ -398,6 +416,9 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     float* cv_gb = cv_gw + (C::kGated ? C::kMyChunks * 32 : 0);
     int acc = 0;
     uint32_t acc_phase = 0;
+    unsigned gtrace_k = 0;
+    const int tslot = ew == 0 ? 1 : (ew == 4 ? 2 : -1);
+#define EPI_TRACE(code) do { if (tslot > 0) GEMM_TRACE(tslot, code); } while (0)
     for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int g, mp, n_blk;
       decode(tile, g, mp, n_blk);
@@ -444,6 +465,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         rs = rsqrtf(fmaxf(s2 / ep.d_true - ln_mean * ln_mean, 0.f) + 1e-5f);
       }
       ptx::mbar_wait(&tmem_full[acc], acc_phase);
+      EPI_TRACE(4);
       ptx::tc_fence_after();
       // LN(x) W + b = rs * acc + (b - rs * mean * u)
       const uint64_t rs2 = f2::make(rs, rs);
@@ -629,6 +651,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
             ptx::tma_store_commit();  // one group per chunk keeps the box rotation exact
           }
         }
+        EPI_TRACE(5);
         if constexpr (C::kResidTma) {
           // the residual box was read before a proxy fence (the store path's, or
           // this one): refill it with the next box of the stream
@@ -686,6 +709,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         if constexpr (kCG == 1) ptx::mbar_arrive(&tmem_empty[acc]);
         else ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tmem_empty[acc]), 0));
       }
+      EPI_TRACE(6);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (epi_leader) ptx::tma_store_wait<0>();

@@ -5,7 +5,7 @@
 
 The capture command (run under gpurun, one GPU) is
     ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-        -k regex:5flame -c 11 -o gpurun_out/prof_full_cfg3 python dev/prof_step.py cfg3 1
+        -k regex:5flame -c 10 -o gpurun_out/prof_full_cfg3 python dev/prof_step.py cfg3 1
 Kernels are labelled by their position in the launch sequence of one pass
 (paper_2509_22681_b200/csrc/flame.cu Pipe::run), which is fixed for a config.
 Writes:
@@ -25,9 +25,9 @@ import subprocess
 from pathlib import Path
 
 # launch order of one id-input pass at L = 1 in bf16 mode
+# (the gated fusion runs inside the FFN W2 epilogue of the last layer)
 ROLES_L1 = ["pda_dedup", "pda_gather", "gemm_kv_hist", "gemm_qkv_cand", "attention_sumi",
-            "gemm_oproj_cand", "gemm_ffn_w1", "gemm_ffn_w2", "gated_fusion", "gemm_expert_w1",
-            "expert_combine"]
+            "gemm_oproj_cand", "gemm_ffn_w1", "gemm_ffn_w2", "gemm_expert_w1", "expert_combine"]
 
 METRICS = {
     "duration_ms": "gpu__time_duration.sum",
