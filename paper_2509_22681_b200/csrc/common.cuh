@@ -183,16 +183,18 @@ __device__ __forceinline__ uint64_t add(uint64_t a, uint64_t b) {
   return d;
 }
 // tanh-form GELU on a pair: hx (1 + tanh(x (k0 + k1 x^2))), hx = x / 2
-__device__ __forceinline__ uint64_t gelu(uint64_t x) {
+// TWICE the tanh-form GELU, x (1 + tanh(x (k0 + k1 x^2))): the 1/2 is folded
+// into every consumer's weights at pack time (FFN W2, expert W2 — exact, a power
+// of two), saving one multiply per element in the GELU epilogues; bf16(2 g) =
+// 2 bf16(g) and (2 g)(w / 2) = g w, so the results are bit-identical.
+__device__ __forceinline__ uint64_t gelu2x(uint64_t x) {
   const uint64_t k0 = make(0.7978845608028654f, 0.7978845608028654f);
   const uint64_t k1 = make(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
-  const uint64_t h = make(0.5f, 0.5f);
   const uint64_t z = mul(x, fma(mul(x, x), k1, k0));
   float z0, z1;
   split(z, z0, z1);
   asm("tanh.approx.f32 %0, %0;" : "+f"(z0));
   asm("tanh.approx.f32 %0, %0;" : "+f"(z1));
-  const uint64_t hx = mul(x, h);
-  return fma(hx, make(z0, z1), hx);
+  return fma(x, make(z0, z1), x);
 }
 }  // namespace f2

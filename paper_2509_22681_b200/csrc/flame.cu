@@ -299,6 +299,10 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
       }
       if (!need(static_cast<long long>(f) * d)) return fail(1, "weights too short (w2)");
       pack_transposed(h.w2, static_cast<size_t>(b) * D * F, D, F, a, f, d, id_d, id_f);
+      if (kFold) {  // the tcgen05 GELU epilogue writes 2 GELU (common.cuh f2::gelu2x)
+        T* w2b = h.w2.data() + static_cast<size_t>(b) * D * F;
+        for (size_t i = 0; i < static_cast<size_t>(D) * F; ++i) w2b[i] = cvt<T>(0.5f * static_cast<float>(w2b[i]));
+      }
       if (!need(d)) return fail(1, "weights too short (b2)");
       for (int i = 0; i < d; ++i) h.b2[static_cast<size_t>(b) * D + i] = static_cast<float>(a[i]);
     }
@@ -338,7 +342,8 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
   for (int i = 0; i < f; ++i) be1[i] = static_cast<float>(a[i]);
   if (!need(static_cast<long long>(f) * tasks)) return fail(1, "weights too short (expert_w2)");
   for (int k = 0; k < f; ++k)
-    for (int t = 0; t < tasks; ++t) we2[static_cast<size_t>(k) * tasks + t] = static_cast<float>(a[static_cast<size_t>(k) * tasks + t]);
+    for (int t = 0; t < tasks; ++t)  // bf16 path: halved for the 2 GELU epilogue (f2::gelu2x)
+      we2[static_cast<size_t>(k) * tasks + t] = static_cast<float>(a[static_cast<size_t>(k) * tasks + t]) * (kSplit ? 0.5f : 1.f);
   std::vector<float> we2p(static_cast<size_t>(F) * 4, 0.f);
   for (int k = 0; k < f; ++k)
     for (int t = 0; t < tasks && t < 4; ++t) we2p[static_cast<size_t>(k) * 4 + t] = we2[static_cast<size_t>(k) * tasks + t];

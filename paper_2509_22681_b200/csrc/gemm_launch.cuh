@@ -61,10 +61,17 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   }
   const int m_tiles = (p.M + gemm::BM - 1) / gemm::BM;
   const int n_tiles = (p.N + BN - 1) / BN;
-  // CTA pairs pay off for long K loops (FFN W2, K = 2048; expert, K = 3d): measured
-  // at cfg3 W2 0.488 -> 0.458 ms.  The K = 512 GEMMs are epilogue-paced and lose a
-  // little to the pair handshake (W1 0.520 -> 0.541 ms), so they run single-CTA.
-  const int ncl = (gemm_cluster_pref() == 2 && m_tiles >= 2 && max_clusters > 0 && p.K >= 1024) ? 2 : 1;
+  // CTA pairs halve each CTA's W-tile traffic from L2, which is what paces the
+  // light-epilogue K = 512 GEMMs (measured at cfg3: QKV 0.367 -> 0.323 ms, K/V of
+  // the history 0.136 -> 0.120 ms).  The GELU / LayerNorm-statistics epilogues are
+  // the limit of their GEMMs instead and lose to the pair handshake below K = 1024
+  // (W1 0.567 -> 0.60 ms), as do all GEMMs with K < 512.
+  static const int pair_min_k_env = [] {  // FLAME_GEMM_PAIR_MINK overrides (A/B)
+    const char* e = getenv("FLAME_GEMM_PAIR_MINK");
+    return e ? atoi(e) : 0;
+  }();
+  const int pair_min_k = pair_min_k_env > 0 ? pair_min_k_env : (C1::kHeavy ? 1024 : 512);
+  const int ncl = (gemm_cluster_pref() == 2 && m_tiles >= 2 && max_clusters > 0 && p.K >= pair_min_k) ? 2 : 1;
   CUtensorMap ta, tb;
   const int ga = p.a_shared ? 1 : p.G;
   if (!make_tmap_bf16_3d(&ta, p.A, p.K, p.M, ga, p.lda * 2, p.a_gstride * 2, gemm::BK, gemm::BM))

@@ -529,8 +529,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
             p1 = f2::add(p1, b1);
           }
           if constexpr ((EPI & EPI_GELU) != 0) {
-            p0 = f2::gelu(p0);
-            p1 = f2::gelu(p1);
+            p0 = f2::gelu2x(p0);  // 2 GELU: consumers hold W / 2
+            p1 = f2::gelu2x(p1);
           }
           if constexpr ((EPI & EPI_RESID) != 0) {
             float4 rr;
