@@ -163,8 +163,7 @@ static cudaError_t launch_gemm_bn(const GemmProblem& p, cudaStream_t s, int num_
 // N output columns: one per (column tile, epilogue-warp share).
 static int gemm_row_parts(int N, int epi) {
   const int bn = N >= 256 ? 256 : 128;
-  const bool heavy = (epi & (EPI_GELU | EPI_LNSTATS | EPI_STATS)) != 0 && (epi & EPI_OUT_F32) == 0;
-  return ((N + bn - 1) / bn) * (heavy ? FLAME_GEMM_HEAVY_WARPS / 4 : 2);
+  return ((N + bn - 1) / bn) * (gemm::gemm_epi_warps(epi) / 4);
 }
 
 // debug: trace (g_gemm_trace) only the which-th GEMM launched after flame_debug_gemm_trace

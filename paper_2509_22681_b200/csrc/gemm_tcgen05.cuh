@@ -125,10 +125,15 @@ constexpr int kSmemBudget = 227 * 1024;
 #ifndef FLAME_GEMM_HEAVY_WARPS
 #define FLAME_GEMM_HEAVY_WARPS 8
 #endif
+// epilogue warps of a variant: FLAME_GEMM_HEAVY_WARPS for the bf16 GELU epilogues,
+// 8 otherwise (host code sizes the row-partial buffers with the same rule)
+__host__ __device__ constexpr int gemm_epi_warps(int epi) {
+  return ((epi & EPI_GELU) != 0 && (epi & EPI_OUT_F32) == 0) ? FLAME_GEMM_HEAVY_WARPS : 8;
+}
 template <int BN, int EPI, int kCG>
 struct Cfg {
   static constexpr bool kHeavy = (EPI & (EPI_GELU | EPI_LNSTATS | EPI_STATS)) != 0;
-  static constexpr int kEpiWarps = (kHeavy && (EPI & EPI_OUT_F32) == 0) ? FLAME_GEMM_HEAVY_WARPS : 8;
+  static constexpr int kEpiWarps = gemm_epi_warps(EPI);
   static constexpr int kEpiPerQuad = kEpiWarps / 4;
   static constexpr int kThreads = 128 + 32 * kEpiWarps;
   static constexpr bool kF32 = (EPI & EPI_OUT_F32) != 0;
