@@ -424,6 +424,34 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     unsigned gtrace_k = 0;
     const int tslot = ew == 0 ? 1 : (ew == 4 ? 2 : -1);
 #define EPI_TRACE(code) do { if (tslot > 0) GEMM_TRACE(tslot, code); } while (0)
+    // per-row epilogue operands of a tile, prefetched one tile ahead
+    constexpr int kMaxPre = (EPI & EPI_LNSTATS) != 0 ? 4 : 0;
+    struct RowOps {
+      float rs;
+      float2 p[kMaxPre > 0 ? kMaxPre : 1];
+    };
+    auto load_row_ops = [&](int t) {
+      RowOps o;
+      o.rs = 1.f;
+#pragma unroll
+      for (int k = 0; k < (kMaxPre > 0 ? kMaxPre : 1); ++k) o.p[k] = make_float2(0.f, 0.f);
+      if (t >= total_tiles) return o;
+      int gg, mpp, nbb;
+      decode(t, gg, mpp, nbb);
+      const int r = min((mpp * ncl + crank) * gemm::BM + wq * 32 + lane, ep.M - 1);
+      if constexpr ((EPI & EPI_ROWSCALE) != 0) o.rs = __ldg(ep.rowscale + gg * ep.rowscale_gstride + r);
+      if constexpr (kMaxPre > 0) {
+        if (ep.stats_parts <= kMaxPre) {
+          const float2* pst = reinterpret_cast<const float2*>(ep.lnstats + gg * ep.lnstats_gstride) +
+                              static_cast<long long>(r) * ep.stats_parts;
+#pragma unroll
+          for (int k = 0; k < kMaxPre; ++k)
+            if (k < ep.stats_parts) o.p[k] = __ldg(pst + k);
+        }
+      }
+      return o;
+    };
+    RowOps row_ops = load_row_ops(tile_at(0));
     for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int g, mp, n_blk;
       decode(tile, g, mp, n_blk);
@@ -444,8 +472,6 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         }
         __syncwarp();
       }
-      // per-row operands (folded-LN rstd / mean) are loaded BEFORE the accumulator
-      // wait: their global-load latency then overlaps this tile's MMAs
       const int row0 = m_blk * gemm::BM + wq * 32;
       // rows past M are clipped by the TMA store; clamp their residual reads
       const int row = min(row0 + lane, ep.M - 1);
@@ -453,18 +479,32 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       // gated fusion: running sum over groups at TMEM columns [2 BN, 3 BN)
       const uint32_t t_gsum = tmem_base + 2 * BN + (static_cast<uint32_t>(wq * 32) << 16);
       const bool g_first = g == 0, g_last = g == groups - 1;
-      float rs = (EPI & EPI_ROWSCALE) ? ep.rowscale[g * ep.rowscale_gstride + row] : 1.f;
+      // per-row operands (rowscale, folded-LN2 partials) were loaded one tile ahead;
+      // queue the next tile's now, so their global-load latency is never exposed
+      const RowOps cur_ops = row_ops;
+      row_ops = load_row_ops(tile_at(it + 1));
+      float rs = 1.f;
       float ln_mean = 0.f;
+      if constexpr ((EPI & EPI_ROWSCALE) != 0) rs = cur_ops.rs;
       if constexpr ((EPI & EPI_LNSTATS) != 0) {
         // combine the producer's per-tile (sum, sumsq) partials in fixed order
-        const float2* pst = reinterpret_cast<const float2*>(ep.lnstats + g * ep.lnstats_gstride) +
-                            static_cast<long long>(row) * ep.stats_parts;
         float s1 = 0.f, s2 = 0.f;
-#pragma unroll 4
-        for (int k = 0; k < ep.stats_parts; ++k) {
-          const float2 p = pst[k];
-          s1 += p.x;
-          s2 += p.y;
+        if (ep.stats_parts <= kMaxPre) {
+#pragma unroll
+          for (int k = 0; k < kMaxPre; ++k) {
+            if (k < ep.stats_parts) {
+              s1 += cur_ops.p[k].x;
+              s2 += cur_ops.p[k].y;
+            }
+          }
+        } else {
+          const float2* pst = reinterpret_cast<const float2*>(ep.lnstats + g * ep.lnstats_gstride) +
+                              static_cast<long long>(row) * ep.stats_parts;
+          for (int k = 0; k < ep.stats_parts; ++k) {
+            const float2 p = pst[k];
+            s1 += p.x;
+            s2 += p.y;
+          }
         }
         ln_mean = s1 / ep.d_true;
         rs = rsqrtf(fmaxf(s2 / ep.d_true - ln_mean * ln_mean, 0.f) + 1e-5f);
