@@ -88,6 +88,12 @@ int flame_create_flmp(const void* flmp_bytes, long long n_bytes, int precision, 
                       FlameCtx** out);
 int flame_destroy(FlameCtx* ctx);
 int flame_set_table(FlameCtx* ctx, const float* host_table, long long num_items, int table_dtype);
+/* Incremental refresh of the device item table: rows [n][hidden_dim] fp32 written
+ * to table[ids[i]] on `stream` (synchronised before return).  Replaces the
+ * reference's per-key cache refresh after SimulatedRemoteStore.mutate
+ * (store.py:104-108, cache.py:170-357) for the device-resident table. */
+int flame_update_table(FlameCtx* ctx, const long long* host_ids, const float* host_rows, long long n,
+                       void* stream);
 
 /* Capacity of one id list in the unique/inverse buffers: max(H_bkt, C_bkt). */
 int flame_exec_list_capacity(int num_blocks, int hb_bkt, int c_bkt);

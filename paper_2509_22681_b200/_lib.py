@@ -20,7 +20,7 @@ INPUT_EMBEDDINGS, INPUT_IDS, INPUT_GATHER_ONLY = 0, 1, 2
 TABLE_BF16, TABLE_FP32 = 0, 1
 
 EXPORTED = (
-    "flame_create", "flame_create_flmp", "flame_destroy", "flame_set_table",
+    "flame_create", "flame_create_flmp", "flame_destroy", "flame_set_table", "flame_update_table",
     "flame_exec_list_capacity", "flame_exec_create", "flame_exec_destroy", "flame_exec_run",
     "flame_exec_capture", "flame_exec_replay", "flame_exec_launch_count", "flame_exec_workspace",
     "flame_exec_profile",
@@ -62,6 +62,7 @@ def load() -> ctypes.CDLL:
             "flame_create_flmp": (I, [P, LL, I, I, ctypes.POINTER(P)]),
             "flame_destroy": (I, [P]),
             "flame_set_table": (I, [P, P, LL, I]),
+            "flame_update_table": (I, [P, P, P, LL, P]),
             "flame_exec_list_capacity": (I, [I, I, I]),
             "flame_exec_create": (I, [P, I, I, I, ctypes.POINTER(FlameIO), ctypes.POINTER(P)]),
             "flame_exec_destroy": (I, [P]),

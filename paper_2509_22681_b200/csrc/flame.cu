@@ -966,6 +966,32 @@ int flame_set_table(FlameCtx* c, const float* host_table, long long num_items, i
   return 0;
 }
 
+int flame_update_table(FlameCtx* c, const long long* host_ids, const float* host_rows, long long n, void* stream) {
+  if (!c || n < 0 || (n > 0 && (!host_ids || !host_rows))) return fail(1, "bad table update arguments");
+  if (!c->table) return fail(1, "no embedding table set (flame_set_table)");
+  if (n == 0) return 0;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long long* d_ids = nullptr;
+  float* d_rows = nullptr;
+  CUDA_TRY(cudaMallocAsync(&d_ids, n * sizeof(long long), s));
+  CUDA_TRY(cudaMallocAsync(&d_rows, n * c->d * sizeof(float), s));
+  CUDA_TRY(cudaMemcpyAsync(d_ids, host_ids, n * sizeof(long long), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_rows, host_rows, n * c->d * sizeof(float), cudaMemcpyHostToDevice, s));
+  const unsigned blocks = static_cast<unsigned>((n * 32 + 255) / 256);
+  if (c->table_dtype == FLAME_TABLE_BF16)
+    table_scatter_rows<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<__nv_bfloat16*>(c->table), c->num_items,
+                                                           c->D, c->d, d_ids, d_rows, static_cast<int>(n));
+  else
+    table_scatter_rows<float><<<blocks, 256, 0, s>>>(static_cast<float*>(c->table), c->num_items, c->D, c->d,
+                                                   d_ids, d_rows, static_cast<int>(n));
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(d_ids, s));
+  CUDA_TRY(cudaFreeAsync(d_rows, s));
+  CUDA_TRY(cudaStreamSynchronize(s));  // host buffers may be reused on return
+  return 0;
+}
+
 int flame_exec_list_capacity(int num_blocks, int hb_bkt, int c_bkt) {
   const int H = num_blocks * hb_bkt;
   return H > c_bkt ? H : c_bkt;

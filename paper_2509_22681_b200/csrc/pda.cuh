@@ -18,6 +18,7 @@
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <type_traits>
 
 namespace flame {
 
@@ -243,6 +244,25 @@ __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
     row = static_cast<long long>(r) * a.l.C_bkt + n + k;
   }
   assemble_row_st<kChunks>(a.o, is_hist, row, z, lane, a.D, a.d_true, RowStats{0.f, 0.f});
+  }
+}
+
+// Incremental refresh of the device item table (changed store rows,
+// e.g. a key whose version was bumped): one warp per updated row, fp32 source
+// rows [n][d] scattered to table[id] (converted to the table dtype, padding
+// columns zeroed).  Ids outside the table are ignored (they stay zero rows).
+template <typename TTab>
+__global__ void table_scatter_rows(TTab* __restrict__ table, long long num_items, int D, int d,
+                                   const long long* __restrict__ ids, const float* __restrict__ rows, int n) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= n) return;
+  const long long id = ids[w];
+  if (id < 0 || id >= num_items) return;
+  for (int c = lane; c < D; c += 32) {
+    const float v = c < d ? rows[static_cast<long long>(w) * d + c] : 0.f;
+    if constexpr (std::is_same<TTab, float>::value) table[id * D + c] = v;
+    else table[id * D + c] = __float2bfloat16_rn(v);
   }
 }
 

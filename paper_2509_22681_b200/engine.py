@@ -82,6 +82,20 @@ class FlameEngine:
             _lib.check(self.lib.flame_set_table(self.handle, t.ctypes.data, t.shape[0], code))
         self.num_items = t.shape[0]
 
+    def update_rows(self, ids, rows: np.ndarray) -> None:
+        """Overwrite table rows ``ids`` with ``rows`` (n, hidden_dim) in place on the
+        device (incremental refresh; ids outside the table are ignored)."""
+        if not self.num_items:
+            raise RuntimeError("no embedding table set (set_table)")
+        i = np.ascontiguousarray(ids, dtype=np.int64).reshape(-1)
+        r = np.ascontiguousarray(rows, dtype=np.float32)
+        if r.shape != (i.size, self.config.hidden_dim):
+            raise ValueError(f"rows must be ({i.size}, {self.config.hidden_dim})")
+        stream = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.flame_update_table(self.handle, i.ctypes.data, r.ctypes.data, i.size,
+                                                   ctypes.c_void_p(stream.cuda_stream)))
+
     def bucket(self, hist_len: int, cand_count: int) -> tuple[int, int]:
         """(hb_bkt, c_bkt) shape bucket for one request (powers of two, capped)."""
         cfg = self.config
@@ -236,10 +250,10 @@ class DeviceExecutor:
             hc[r, :c] = cand
             hl.append(h)
             cl.append(c)
-        self._set_meta(hl, cl)
+        n = self._set_meta(hl, cl)
         with torch.cuda.stream(self.stream):
-            self.hist_emb.copy_(self.h_hist, non_blocking=True)
-            self.cand_emb.copy_(self.h_cand, non_blocking=True)
+            self.hist_emb[:n].copy_(self.h_hist[:n], non_blocking=True)
+            self.cand_emb[:n].copy_(self.h_cand[:n], non_blocking=True)
             self._upload_meta()
 
     def stage_ids(self, requests) -> None:
@@ -255,10 +269,11 @@ class DeviceExecutor:
             hc[r, :c] = cand
             hl.append(h)
             cl.append(c)
-        self._set_meta(hl, cl)
+        n = self._set_meta(hl, cl)
         with torch.cuda.stream(self.stream):
-            self.hist_ids.copy_(self.h_hist_ids, non_blocking=True)
-            self.cand_ids.copy_(self.h_cand_ids, non_blocking=True)
+            # only the slots in use cross PCIe (the kernels skip the others)
+            self.hist_ids[:n].copy_(self.h_hist_ids[:n], non_blocking=True)
+            self.cand_ids[:n].copy_(self.h_cand_ids[:n], non_blocking=True)
             self._upload_meta()
 
     def _upload_meta(self) -> None:

@@ -1,0 +1,90 @@
+"""Device request path (paper_2509_22681_b200.service): the reference service
+tests (tests/test_service.py) re-run against the HBM item table + PDA + DSO."""
+
+import numpy as np
+import pytest
+
+import paper_2509_22681_b200 as fb
+from oracle import flame_oracle as orc
+from paper_2509_22681_b200.pda import item_embedding
+from paper_2509_22681_b200.service import (DeviceService, RequestError, ScoreRequest, ServiceClosedError)
+
+pytestmark = pytest.mark.gpu
+
+CFG = fb.ModelConfig(32, 8, 2, 1, 64, 2, 64, 32, seed=5)
+NUM_ITEMS = 400
+
+
+def request_of(hist, cand):
+    return ScoreRequest(user_id=1, history_item_ids=np.asarray(list(hist), dtype=np.int64),
+                        candidate_item_ids=np.asarray(list(cand), dtype=np.int64))
+
+
+def resolve(ids, versions=None):
+    """Reference resolve_embeddings (service.py:97-108) over the store function."""
+    versions = versions or {}
+    rows = [item_embedding(1234, int(i), versions.get(int(i), 0), CFG.hidden_dim) if 0 <= i < NUM_ITEMS
+            else np.zeros(CFG.hidden_dim) for i in ids]
+    return np.asarray(rows).reshape(len(ids), CFG.hidden_dim)
+
+
+@pytest.fixture(scope="module")
+def service(gpu):
+    s = DeviceService(CFG, num_items=NUM_ITEMS, target_rows=256)
+    yield s
+    if not s._closed:
+        s.close()
+
+
+def test_pipeline_matches_reference_forward(service):
+    # reference tests/test_service.py:42-51 (pipeline == direct forward)
+    req = request_of(range(16), range(200, 221))
+    resp = service.handle_request(req)
+    want = orc.model_forward(resolve(req.history_item_ids), resolve(req.candidate_item_ids),
+                             service.params, CFG)
+    assert resp.scores.shape == (21, 2)
+    assert np.abs(resp.scores - want).max() <= 2e-2
+    assert resp.overall_latency_ms >= resp.compute_latency_ms > 0
+
+
+def test_identical_requests_identical_scores(service):
+    req = request_of(range(12), range(50, 57))
+    np.testing.assert_array_equal(service.handle_request(req).scores, service.handle_request(req).scores)
+
+
+def test_batch_equals_single_and_unknown_ids_are_zero_rows(service):
+    rng = np.random.default_rng(3)
+    reqs = [request_of(rng.integers(-5, NUM_ITEMS + 50, 2 * int(rng.integers(0, 33))),
+                       rng.integers(-5, NUM_ITEMS + 50, int(rng.integers(1, 33)))) for _ in range(12)]
+    batch = service.handle_batch(reqs)
+    for r, b in zip(reqs, batch):
+        np.testing.assert_array_equal(b.scores, service.handle_request(r).scores)
+        want = orc.model_forward(resolve(r.history_item_ids), resolve(r.candidate_item_ids), service.params, CFG)
+        assert np.abs(b.scores - want).max() <= 2e-2
+
+
+def test_mutate_refreshes_device_rows(service):
+    req = request_of(range(8), range(100, 104))
+    before = service.handle_request(req).scores
+    service.mutate([101, 3])
+    after = service.handle_request(req).scores
+    assert not np.array_equal(before, after)
+    versions = {101: 1, 3: 1}
+    want = orc.model_forward(resolve(req.history_item_ids, versions), resolve(req.candidate_item_ids, versions),
+                             service.params, CFG)
+    assert np.abs(after - want).max() <= 2e-2
+
+
+def test_validation_metrics_and_close(service):
+    for bad in (request_of(range(8), []), request_of(range(7), range(3)), request_of(range(8), range(33)),
+                request_of(range(66), range(3))):
+        with pytest.raises(RequestError):
+            service.handle_request(bad)
+    n0 = service.pairs_processed
+    service.handle_batch([request_of(range(8), range(5)), request_of(range(8), range(16))])
+    assert service.pairs_processed == n0 + 21
+    snap = service.metrics_snapshot()
+    assert snap["requests_total"] >= 2 and snap["overall_ms"]["count"] == snap["requests_total"]
+    service.close()
+    with pytest.raises(ServiceClosedError):
+        service.handle_request(request_of(range(8), range(3)))
