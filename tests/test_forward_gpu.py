@@ -152,3 +152,28 @@ def test_bf16_and_fp32_paths_agree_at_cfg2(gpu):
     a = fb.model_forward(hist, cand, params, cfg, precision="bf16")
     b = fb.model_forward(hist, cand, params, cfg, precision="fp32")
     assert np.abs(a - b).max() <= 2e-2
+
+
+def test_full_size_batch_invariance_cfg3_ids(gpu):
+    """BASELINE cfg3 shape (8 blocks, d=512, H=2048, C=512) through the id path:
+    an 8-request batch equals the same requests split 3 + 5 (partially filled
+    executors: the device-side active count skips the unused slots) and one at a
+    time, bit for bit; a duplicated request scores identically."""
+    from paper_2509_22681_b200.pda import build_item_table
+
+    cfg = fb.ModelConfig(512, 64, 8, 1, 2048, 2, 2048, 512, seed=0)
+    eng = fb.FlameEngine(fb.init_params(cfg), cfg, "bf16")
+    eng.set_table(build_item_table(3000, 512), dtype="fp32")
+    rng = np.random.default_rng(2509)
+    reqs = [(rng.integers(0, 3000, 2048), rng.integers(0, 3000, int(c))) for c in (512, 17, 512, 300, 511, 64, 512, 1)]
+    reqs[6] = reqs[0]
+    ex8 = eng.executor(8, 256, 512, with_ids=True)
+    full = ex8.score_ids(reqs)
+    split = ex8.score_ids(reqs[:3]) + ex8.score_ids(reqs[3:])
+    one = [ex8.score_ids([r])[0] for r in reqs[:2]]
+    for a, b in zip(full, split):
+        np.testing.assert_array_equal(a, b)
+    for a, b in zip(full[:2], one):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(full[0], full[6])
+    assert all(np.isfinite(s).all() and s.shape == (len(c), 2) for (_, c), s in zip(reqs, full))
