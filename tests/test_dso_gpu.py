@@ -125,3 +125,23 @@ def test_bucket_scheduler_ring_and_ids(gpu):
     for g, w, c in zip(got, want, counts):
         assert g.shape == (int(c), 2)
         np.testing.assert_array_equal(g, w)
+
+
+def test_score_stream_matches_score(gpu):
+    """Streaming several batches (next batch submitted before the previous is
+    collected) returns, per batch and in order, exactly what score() returns."""
+    cfg = fb.ModelConfig(32, 8, 2, 1, 64, 2, 64, 128, seed=9)
+    params = fb.init_params(cfg)
+    eng = fb.FlameEngine(params, cfg, "bf16")
+    sched = BucketScheduler(eng, target_rows=256, executors_per_bucket=2)
+    rng = np.random.default_rng(4)
+    batches = []
+    for _ in range(4):
+        counts = rng.integers(1, 129, int(rng.integers(3, 9)))
+        batches.append([(rng.uniform(-1, 1, (64, 32)), rng.uniform(-1, 1, (int(c), 32))) for c in counts])
+    streamed = list(sched.score_stream(batches))
+    assert len(streamed) == len(batches)
+    for batch, got in zip(batches, streamed):
+        want = sched.score(batch)
+        for g, w in zip(got, want):
+            np.testing.assert_array_equal(g, w)
