@@ -94,6 +94,12 @@ int flame_set_table(FlameCtx* ctx, const float* host_table, long long num_items,
  * (store.py:104-108, cache.py:170-357) for the device-resident table. */
 int flame_update_table(FlameCtx* ctx, const long long* host_ids, const float* host_rows, long long n,
                        void* stream);
+/* Same, from raw store feature values in the reference wire format (store.py:66-78:
+ * hidden_dim little-endian float64 + filler): value i occupies value_len[i] bytes at
+ * host_values + i * value_stride; values shorter than hidden_dim * 8 bytes decode to
+ * zero rows (decode_embedding).  The decode runs on the device. */
+int flame_update_table_values(FlameCtx* ctx, const long long* host_ids, const void* host_values,
+                              long long value_stride, const int* host_value_len, long long n, void* stream);
 
 /* Capacity of one id list in the unique/inverse buffers: max(H_bkt, C_bkt). */
 int flame_exec_list_capacity(int num_blocks, int hb_bkt, int c_bkt);

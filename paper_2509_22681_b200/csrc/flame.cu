@@ -992,6 +992,39 @@ int flame_update_table(FlameCtx* c, const long long* host_ids, const float* host
   return 0;
 }
 
+int flame_update_table_values(FlameCtx* c, const long long* host_ids, const void* host_values,
+                              long long value_stride, const int* host_value_len, long long n, void* stream) {
+  if (!c || n < 0 || value_stride < 0 || (n > 0 && (!host_ids || !host_values || !host_value_len)))
+    return fail(1, "bad table update arguments");
+  if (!c->table) return fail(1, "no embedding table set (flame_set_table)");
+  if (n == 0) return 0;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long long* d_ids = nullptr;
+  uint8_t* d_vals = nullptr;
+  int* d_len = nullptr;
+  CUDA_TRY(cudaMallocAsync(&d_ids, n * sizeof(long long), s));
+  CUDA_TRY(cudaMallocAsync(&d_vals, n * value_stride + 1, s));
+  CUDA_TRY(cudaMallocAsync(&d_len, n * sizeof(int), s));
+  CUDA_TRY(cudaMemcpyAsync(d_ids, host_ids, n * sizeof(long long), cudaMemcpyHostToDevice, s));
+  if (value_stride > 0) CUDA_TRY(cudaMemcpyAsync(d_vals, host_values, n * value_stride, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_len, host_value_len, n * sizeof(int), cudaMemcpyHostToDevice, s));
+  const unsigned blocks = static_cast<unsigned>((n * 32 + 255) / 256);
+  if (c->table_dtype == FLAME_TABLE_BF16)
+    table_decode_values<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<__nv_bfloat16*>(c->table), c->num_items,
+                                                            c->D, c->d, d_ids, d_vals, value_stride, d_len,
+                                                            static_cast<int>(n));
+  else
+    table_decode_values<float><<<blocks, 256, 0, s>>>(static_cast<float*>(c->table), c->num_items, c->D, c->d,
+                                                    d_ids, d_vals, value_stride, d_len, static_cast<int>(n));
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(d_ids, s));
+  CUDA_TRY(cudaFreeAsync(d_vals, s));
+  CUDA_TRY(cudaFreeAsync(d_len, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
 int flame_exec_list_capacity(int num_blocks, int hb_bkt, int c_bkt) {
   const int H = num_blocks * hb_bkt;
   return H > c_bkt ? H : c_bkt;

@@ -266,4 +266,32 @@ __global__ void table_scatter_rows(TTab* __restrict__ table, long long num_items
   }
 }
 
+// Store feature values straight into the table: the reference's wire format
+// (store.py:66-78 encode_feature_value / decode_embedding) is d little-endian
+// float64 followed by filler up to bytes_per_value; a value shorter than d * 8
+// bytes (e.g. empty) decodes to a zero row.  One warp per value.
+template <typename TTab>
+__global__ void table_decode_values(TTab* __restrict__ table, long long num_items, int D, int d,
+                                    const long long* __restrict__ ids, const uint8_t* __restrict__ values,
+                                    long long value_stride, const int* __restrict__ value_len, int n) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= n) return;
+  const long long id = ids[w];
+  if (id < 0 || id >= num_items) return;
+  const bool ok = value_len[w] >= d * 8;
+  const uint8_t* v = values + static_cast<long long>(w) * value_stride;
+  for (int c = lane; c < D; c += 32) {
+    double x = 0.0;
+    if (ok && c < d) {
+      unsigned long long bits = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) bits |= static_cast<unsigned long long>(v[c * 8 + b]) << (8 * b);  // little endian
+      x = __longlong_as_double(static_cast<long long>(bits));
+    }
+    if constexpr (std::is_same<TTab, float>::value) table[id * D + c] = static_cast<float>(x);
+    else table[id * D + c] = __float2bfloat16_rn(static_cast<float>(x));
+  }
+}
+
 }  // namespace flame

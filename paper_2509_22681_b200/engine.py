@@ -96,6 +96,28 @@ class FlameEngine:
             _lib.check(self.lib.flame_update_table(self.handle, i.ctypes.data, r.ctypes.data, i.size,
                                                    ctypes.c_void_p(stream.cuda_stream)))
 
+    def update_values(self, ids, values) -> None:
+        """Overwrite table rows ``ids`` from raw store feature values (bytes in the
+        reference wire format, store.py:66-78), decoded on the device; short or
+        empty values give zero rows."""
+        if not self.num_items:
+            raise RuntimeError("no embedding table set (set_table)")
+        i = np.ascontiguousarray(ids, dtype=np.int64).reshape(-1)
+        if len(values) != i.size:
+            raise ValueError("one value per id")
+        stride = max([len(v) for v in values] + [8])
+        stride = (stride + 7) // 8 * 8
+        buf = np.zeros((i.size, stride), dtype=np.uint8)
+        lens = np.zeros(i.size, dtype=np.int32)
+        for k, v in enumerate(values):
+            buf[k, :len(v)] = np.frombuffer(v, dtype=np.uint8)
+            lens[k] = len(v)
+        stream = torch.cuda.current_stream(self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.flame_update_table_values(self.handle, i.ctypes.data, buf.ctypes.data, stride,
+                                                          lens.ctypes.data, i.size,
+                                                          ctypes.c_void_p(stream.cuda_stream)))
+
     def bucket(self, hist_len: int, cand_count: int) -> tuple[int, int]:
         """(hb_bkt, c_bkt) shape bucket for one request (powers of two, capped)."""
         cfg = self.config

@@ -168,6 +168,13 @@ class DeviceService:
         with self._lock:
             self.engine.update_rows(np.asarray(ids, dtype=np.int64), rows)
 
+    def refresh_values(self, item_ids, values) -> None:
+        """Write raw store feature values (reference wire format, store.py:66-78:
+        float64 LE embedding + filler; empty -> zero row) into the device table,
+        decoded on the GPU — the path a store feed / cache refresh would use."""
+        with self._lock:
+            self.engine.update_values(np.asarray(item_ids, dtype=np.int64), list(values))
+
     # -- observability / lifecycle --------------------------------------------
 
     def metrics_snapshot(self) -> dict:

@@ -88,3 +88,21 @@ def test_validation_metrics_and_close(service):
     service.close()
     with pytest.raises(ServiceClosedError):
         service.handle_request(request_of(range(8), range(3)))
+
+
+def test_refresh_from_store_wire_values(gpu):
+    """Raw store values (float64 LE + filler, store.py:66-78) decoded on the device;
+    an empty value gives a zero row, as decode_embedding does."""
+    svc = DeviceService(CFG, num_items=NUM_ITEMS, target_rows=256)
+    d = CFG.hidden_dim
+    new_emb = np.linspace(-1, 1, d)
+    values = [new_emb.astype("<f8").tobytes() + b"\x00" * (512 - 8 * d), b""]
+    svc.refresh_values([7, 9], values)
+    req = request_of(range(8), [7, 9, 11])
+    got = svc.handle_request(req).scores
+    hist = resolve(req.history_item_ids)
+    hist[7] = new_emb
+    cand = np.stack([new_emb, np.zeros(d), resolve([11])[0]])
+    want = orc.model_forward(hist, cand, svc.params, CFG)
+    assert np.abs(got - want).max() <= 2e-2
+    svc.close()
