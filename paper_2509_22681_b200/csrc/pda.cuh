@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kPdaThreads) pda_dedup(PdaLists a) {
   for (int k = 2; k <= P; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
-        const int i = (t / j) * 2 * j + (t % j);
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // (t / j) * 2j + t % j, j a power of two
         const int ixj = i + j;
         const bool up = (i & k) == 0;
         const long long ki = key[i], kj = key[ixj];
