@@ -84,9 +84,15 @@ __global__ void __launch_bounds__(kPdaThreads) pda_dedup(PdaLists a) {
           pos[i] = pj; pos[ixj] = pi;
         }
       }
-      __syncthreads();
+      // a pass with j <= 32 only touches the 64-element block of its warp, so two
+      // such passes in a row need only a warp barrier (the next pass is j / 2, or
+      // j = k at the start of the next stage)
+      const int jn = j > 1 ? (j >> 1) : k;
+      if (j >= 64 || jn >= 64) __syncthreads();
+      else __syncwarp();
     }
   }
+  __syncthreads();
   // flags + inclusive scan (each thread owns a contiguous segment)
   const int per = (P + blockDim.x - 1) / blockDim.x;
   const int s0 = threadIdx.x * per;
