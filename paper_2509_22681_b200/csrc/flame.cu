@@ -53,6 +53,32 @@ int fail(int code, const std::string& msg) {
 
 inline int pad_to(int x, int m) { return (x + m - 1) / m * m; }
 
+template <int kThreads, int kItems>
+cudaError_t launch_dedup_t(const PdaLists& l, int lists, cudaStream_t s) {
+  using Sort = cub::BlockRadixSort<unsigned long long, kThreads, kItems, int>;
+  constexpr size_t kSort = sizeof(typename Sort::TempStorage);
+  constexpr size_t kArrays = static_cast<size_t>(kThreads) * kItems * 16;
+  constexpr size_t kSmem = kSort > kArrays ? kSort : kArrays;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(pda_dedup<kThreads, kItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  pda_dedup<kThreads, kItems><<<lists, kThreads, kSmem, s>>>(l);
+  return cudaGetLastError();
+}
+
+// lists of up to `cap` ids: the smallest radix-sort shape that holds them
+inline cudaError_t launch_dedup_shape(const PdaLists& l, int cap, int lists, cudaStream_t s) {
+  if (cap <= 512) return launch_dedup_t<64, 8>(l, lists, s);
+  if (cap <= 1024) return launch_dedup_t<128, 8>(l, lists, s);
+  if (cap <= 2048) return launch_dedup_t<256, 8>(l, lists, s);
+  if (cap <= 4096) return launch_dedup_t<512, 8>(l, lists, s);
+  return launch_dedup_t<1024, 8>(l, lists, s);
+}
+
 struct LayerW {
   void* wqkv = nullptr;  // [G][3DA][D]
   void* wo = nullptr;    // [G][D][DA]
@@ -586,6 +612,12 @@ struct Pipe {
     return check();
   }
 
+  int launch_dedup(const PdaLists& l, int cap, int lists, cudaStream_t st) {
+    cudaError_t err = launch_dedup_shape(l, cap, lists, st);
+    if (err != cudaSuccess) return fail(2, std::string("pda_dedup: ") + cudaGetErrorString(err));
+    return 0;
+  }
+
   AssembleOut assemble_out() const {
     AssembleOut o{};
     o.Eh = e->Eh;  // null unless needed (history residual of L >= 2, fp32 mode)
@@ -619,17 +651,9 @@ struct Pipe {
     l.inverse = e->io.inverse ? e->io.inverse : e->inverse_ws;
     l.n_unique = e->io.n_unique ? e->io.n_unique : e->nuniq_ws;
     l.spos = e->spos; l.ustart = e->ustart; l.cap = e->cap; l.active = e->io.active;
-    int P = 1;
-    while (P < e->cap) P <<= 1;
-    const int smem = P * 16;
-    static int smem_set = 0;
-    if (smem > smem_set) {
-      cudaFuncSetAttribute(pda_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      smem_set = smem;
-    }
+    // dedup: one CTA per list, radix sort sized to the list capacity
     mark("pda_dedup", 0.0, static_cast<double>(e->R) * (e->H_bkt + e->c_bkt) * (8.0 + 8.0 + 8.0 + 8.0));
-    const int dthreads = P / 2 < 64 ? 64 : (P / 2 > kPdaThreads ? kPdaThreads : P / 2);
-    pda_dedup<<<2 * e->R, dthreads, smem, s>>>(l);
+    if (int rc = launch_dedup(l, e->cap, 2 * e->R, s)) return rc;
     if (int rc = check()) return rc;
     {
       PdaGatherArgs g{};

@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <type_traits>
+#include <cub/block/block_radix_sort.cuh>
 
 namespace flame {
 
@@ -45,8 +46,16 @@ __device__ __forceinline__ bool pair_less(long long ka, int pa, long long kb, in
   return ka < kb || (ka == kb && pa < pb);
 }
 
-__global__ void __launch_bounds__(kPdaThreads) pda_dedup(PdaLists a) {
-  extern __shared__ uint8_t smem_raw[];
+// Sort phase: cub::BlockRadixSort of (id, position) pairs, kThreads x kItems =
+// the list capacity.  Radix sort is stable, so equal ids keep ascending positions
+// (the (id, position) order np.unique's inverse needs).  When every id of the list
+// is non-negative only the bits up to the largest id are sorted (item ids < 2^17
+// at 100k items: 5 passes instead of 16).
+template <int kThreads, int kItems>
+__global__ void __launch_bounds__(kThreads) pda_dedup(PdaLists a) {
+  using Sort = cub::BlockRadixSort<unsigned long long, kThreads, kItems, int>;
+  constexpr int P = kThreads * kItems;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
   const int list = blockIdx.x;
   const bool is_hist = list < a.R;
   const int r = is_hist ? list : list - a.R;
@@ -57,40 +66,45 @@ __global__ void __launch_bounds__(kPdaThreads) pda_dedup(PdaLists a) {
   const int n = is_hist ? a.hist_len[r] : a.cand_len[r];
   const long long* ids = is_hist ? a.hist_ids + static_cast<long long>(r) * a.H_bkt
                                  : a.cand_ids + static_cast<long long>(r) * a.C_bkt;
-  int P = 1;
-  while (P < n) P <<= 1;
+  __shared__ unsigned long long s_max;
+  __shared__ int warp_tot[32];
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  long long raw[kItems];
+  bool neg = false;
+  unsigned long long mx = 0;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int i = threadIdx.x * kItems + k;
+    raw[k] = i < n ? ids[i] : 0;
+    neg |= raw[k] < 0;
+    mx = raw[k] > static_cast<long long>(mx) ? static_cast<unsigned long long>(raw[k]) : mx;
+  }
+  const bool any_neg = __syncthreads_or(neg);
+  if (!any_neg && mx) atomicMax(&s_max, mx);
+  __syncthreads();
+  const int end_bit = any_neg ? 64 : (s_max == 0 ? 1 : 64 - __clzll(s_max));
+  const unsigned long long pad = end_bit == 64 ? ~0ull : ((1ull << end_bit) - 1);
+  unsigned long long keys[kItems];
+  int vals[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int i = threadIdx.x * kItems + k;
+    const unsigned long long u = static_cast<unsigned long long>(raw[k]);
+    keys[k] = i < n ? (any_neg ? u ^ 0x8000000000000000ull : u) : pad;
+    vals[k] = i;
+  }
+  Sort(*reinterpret_cast<typename Sort::TempStorage*>(smem_raw)).Sort(keys, vals, 0, end_bit);
+  __syncthreads();  // the key / pos arrays alias the sort's temp storage
   long long* key = reinterpret_cast<long long*>(smem_raw);
   int* pos = reinterpret_cast<int*>(key + P);
   int* rank = pos + P;
-  __shared__ int warp_tot[32];
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    key[i] = i < n ? ids[i] : INT64_MAX;
-    pos[i] = i;
-  }
-  __syncthreads();
-  // bitonic sort, ascending by (id, position): one compare-exchange pair per
-  // thread per pass (P / 2 pairs; the block is sized to the bucket's P / 2)
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
-        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // (t / j) * 2j + t % j, j a power of two
-        const int ixj = i + j;
-        const bool up = (i & k) == 0;
-        const long long ki = key[i], kj = key[ixj];
-        const int pi = pos[i], pj = pos[ixj];
-        const bool gt = pair_less(kj, pj, ki, pi);
-        if (gt == up) {
-          key[i] = kj; key[ixj] = ki;
-          pos[i] = pj; pos[ixj] = pi;
-        }
-      }
-      // a pass with j <= 32 only touches the 64-element block of its warp, so two
-      // such passes in a row need only a warp barrier (the next pass is j / 2, or
-      // j = k at the start of the next stage)
-      const int jn = j > 1 ? (j >> 1) : k;
-      if (j >= 64 || jn >= 64) __syncthreads();
-      else __syncwarp();
-    }
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int i = threadIdx.x * kItems + k;  // blocked arrangement: sorted order
+    key[i] = vals[k] < n ? static_cast<long long>(any_neg ? keys[k] ^ 0x8000000000000000ull : keys[k])
+                         : INT64_MAX;
+    pos[i] = vals[k];
   }
   __syncthreads();
   // flags + inclusive scan (each thread owns a contiguous segment)
