@@ -160,6 +160,9 @@ struct FlameExec {
   int stat_parts = 0;
   int* spos = nullptr;
   int* ustart = nullptr;
+  int2* work = nullptr;   // PDA gather work items [2R][wcap]
+  int* n_work = nullptr;  // [2R]
+  int wcap = 0;
   long long* unique_ws = nullptr;
   long long* inverse_ws = nullptr;
   int* nuniq_ws = nullptr;
@@ -651,6 +654,7 @@ struct Pipe {
     l.inverse = e->io.inverse ? e->io.inverse : e->inverse_ws;
     l.n_unique = e->io.n_unique ? e->io.n_unique : e->nuniq_ws;
     l.spos = e->spos; l.ustart = e->ustart; l.cap = e->cap; l.active = e->io.active;
+    l.work = e->work; l.n_work = e->n_work; l.wcap = e->wcap;
     // dedup: one CTA per list, radix sort sized to the list capacity
     mark("pda_dedup", 0.0, static_cast<double>(e->R) * (e->H_bkt + e->c_bkt) * (8.0 + 8.0 + 8.0 + 8.0));
     if (int rc = launch_dedup(l, e->cap, 2 * e->R, s)) return rc;
@@ -659,9 +663,9 @@ struct Pipe {
       PdaGatherArgs g{};
       g.l = l; g.table = c->table; g.num_items = c->num_items; g.D = c->D; g.d_true = c->d; g.G = c->G;
       g.hb_bkt = e->hb_bkt; g.o = assemble_out();
-      // one warp per unique id, plus one per padding row (together <= the list
-      // capacity); up to 4 of them per warp
-      dim3 grid(static_cast<unsigned>((e->cap + 31) / 32), 2 * e->R);
+      // one warp per work item (a <= 32-position piece of a unique id's run) plus one
+      // per padding row (together <= wcap); up to 4 of them per warp
+      dim3 grid(static_cast<unsigned>((e->wcap + 31) / 32), 2 * e->R);
       // rows out + table rows read (upper bound: one per position); candidates also get fp32
       const double tab = c->table_dtype == FLAME_TABLE_BF16 ? 2.0 : 4.0;
       mark("pda_gather", 0.0, static_cast<double>(e->R) * c->D *
@@ -1103,6 +1107,9 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
   e->He = (fold && c->tasks <= 4) ? nullptr : A(e->Rc * F * 4);
   e->spos = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
   e->ustart = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
+  e->wcap = cap + cap / kRunPiece + 1;
+  e->work = static_cast<int2*>(A(2 * static_cast<size_t>(R) * e->wcap * 8));
+  e->n_work = static_cast<int*>(A(2 * static_cast<size_t>(R) * 4));
   e->unique_ws = static_cast<long long*>(A(2 * static_cast<size_t>(R) * cap * 8));
   e->inverse_ws = static_cast<long long*>(A(2 * static_cast<size_t>(R) * cap * 8));
   e->nuniq_ws = static_cast<int*>(A(2 * static_cast<size_t>(R) * 4));

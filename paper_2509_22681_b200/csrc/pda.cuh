@@ -24,6 +24,7 @@
 namespace flame {
 
 constexpr int kPdaThreads = 1024;
+constexpr int kRunPiece = 32;  // positions one gather warp writes per work item
 constexpr int kPdaMaxList = 8192;  // ids per list handled by one CTA (cfg5: 8184)
 
 struct PdaLists {
@@ -38,6 +39,10 @@ struct PdaLists {
   int* n_unique;       // [2R]
   int* spos;           // [2R][cap] positions in sorted order
   int* ustart;         // [2R][cap] run start (index into spos) of each unique id
+  int2* work;          // [2R][wcap] gather work items (unique index, first sorted position):
+                       // each unique id's run split into pieces of <= kRunPiece positions
+  int* n_work;         // [2R]
+  int wcap;            // cap + cap / kRunPiece + 1
   int cap;             // max(H_bkt, C_bkt)
   const int* active;   // [1] requests in use (null: all R); lists of unused slots are skipped
 };
@@ -60,7 +65,10 @@ __global__ void __launch_bounds__(kThreads) pda_dedup(PdaLists a) {
   const bool is_hist = list < a.R;
   const int r = is_hist ? list : list - a.R;
   if (a.active != nullptr && r >= __ldg(a.active)) {
-    if (threadIdx.x == 0) a.n_unique[list] = 0;
+    if (threadIdx.x == 0) {
+      a.n_unique[list] = 0;
+      a.n_work[list] = 0;
+    }
     return;
   }
   const int n = is_hist ? a.hist_len[r] : a.cand_len[r];
@@ -140,17 +148,76 @@ __global__ void __launch_bounds__(kThreads) pda_dedup(PdaLists a) {
   long long* inv = a.inverse + static_cast<long long>(list) * a.cap;
   int* sp = a.spos + static_cast<long long>(list) * a.cap;
   int* us = a.ustart + static_cast<long long>(list) * a.cap;
-  for (int i = s0; i < min(s0 + per, n); ++i) {
-    const int rk = rank[i] + offset - 1;  // unique index of sorted element i
-    const bool first = (i == 0 || key[i] != key[i - 1]);
-    if (first) {
-      uq[rk] = key[i];
-      us[rk] = i;
+  int first_rk[kItems];  // unique index of this thread's run starts (-1: not a start)
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int i = s0 + k;
+    first_rk[k] = -1;
+    if (i < n) {
+      const int rk = rank[i] + offset - 1;  // unique index of sorted element i
+      if (i == 0 || key[i] != key[i - 1]) {
+        uq[rk] = key[i];
+        us[rk] = i;
+        first_rk[k] = rk;
+      }
+      inv[pos[i]] = rk;
+      sp[i] = pos[i];
     }
-    inv[pos[i]] = rk;
-    sp[i] = pos[i];
   }
   if (threadIdx.x == blockDim.x - 1) a.n_unique[list] = offset + local;
+
+  // gather work list: a Zipf-hot id's run (hundreds of positions) would otherwise
+  // be written by one warp while the rest of the grid idles; cut every run into
+  // pieces of <= kRunPiece positions (run starts staged in smem over `rank`)
+  __syncthreads();
+  const int nu = warp_tot[blockDim.x / 32 - 1];
+  int* rs = rank;  // rs[rk] = first sorted position of unique rk (rank[] is consumed)
+#pragma unroll
+  for (int k = 0; k < kItems; ++k)
+    if (first_rk[k] >= 0) rs[first_rk[k]] = s0 + k;
+  __syncthreads();
+  // pieces per unique (kItems consecutive uniques per thread), block scan, emit
+  int pcs[kItems];
+  int plocal = 0;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int rk = threadIdx.x * kItems + k;
+    int c = 0;
+    if (rk < nu) {
+      const int len = (rk + 1 < nu ? rs[rk + 1] : n) - rs[rk];
+      c = (len + kRunPiece - 1) / kRunPiece;
+    }
+    pcs[k] = c;
+    plocal += c;
+  }
+  int pincl = plocal;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, pincl, o);
+    if (lane >= o) pincl += t;
+  }
+  __syncthreads();  // warp_tot reused
+  if (lane == 31) warp_tot[w] = pincl;
+  __syncthreads();
+  if (w == 0) {
+    int v = lane < (blockDim.x / 32) ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    warp_tot[lane] = v;
+  }
+  __syncthreads();
+  int woff = (pincl - plocal) + (w > 0 ? warp_tot[w - 1] : 0);
+  int2* wk = a.work + static_cast<long long>(list) * a.wcap;
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const int rk = threadIdx.x * kItems + k;
+    for (int c = 0; c < pcs[k]; ++c) wk[woff + c] = make_int2(rk, rs[rk] + c * kRunPiece);
+    woff += pcs[k];
+  }
+  if (threadIdx.x == blockDim.x - 1) a.n_work[list] = woff;
 }
 
 template <typename TTab>
@@ -211,10 +278,11 @@ __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
   if (a.l.active != nullptr && r >= __ldg(a.l.active)) return;  // unused slot: its rows are never read
   const int n = is_hist ? a.l.hist_len[r] : a.l.cand_len[r];
   const int nu = a.l.n_unique[list];
+  const int nw = a.l.n_work[list];
   const int lane = threadIdx.x % 32;
   const int hb = is_hist ? n / a.G : 0;
   const int pad_rows = is_hist ? a.G * (a.hb_bkt - hb) : (a.l.C_bkt - n);
-  const int work = nu + pad_rows;  // <= list capacity
+  const int work = nw + pad_rows;
   const int stride = gridDim.x * (blockDim.x / 32);
   for (int u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; u < work; u += stride) {
   auto row_of = [&](int p) -> long long {  // destination row of list position p
@@ -224,13 +292,15 @@ __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
     }
     return static_cast<long long>(r) * a.l.C_bkt + p;
   };
-  if (u < nu) {
+  if (u < nw) {
+    // one piece (<= kRunPiece positions) of one unique id's run
     const long long* uq = a.l.unique + static_cast<long long>(list) * a.l.cap;
     const int* sp = a.l.spos + static_cast<long long>(list) * a.l.cap;
     const int* us = a.l.ustart + static_cast<long long>(list) * a.l.cap;
-    const long long id = uq[u];
-    const int b = us[u];
-    const int e = (u + 1 < nu) ? us[u + 1] : n;
+    const int2 wi = a.l.work[static_cast<long long>(list) * a.l.wcap + u];
+    const long long id = uq[wi.x];
+    const int b = wi.y;
+    const int e = min(b + kRunPiece, (wi.x + 1 < nu) ? us[wi.x + 1] : n);
     const bool known = id >= 0 && id < a.num_items;
     const TTab* table = reinterpret_cast<const TTab*>(a.table) + (known ? id : 0) * a.D;
     float4 v[kChunks];
@@ -239,19 +309,15 @@ __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
       const int c = (k * 32 + lane) * 4;
       v[k] = (known && c < a.D) ? load_row4<TTab>(table, c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    int pos = b + lane < e ? sp[b + lane] : 0;  // first 32 positions of the run, in flight with the row
+    const int pos = b + lane < e ? sp[b + lane] : 0;  // the piece's positions, in flight with the row
     const RowStats st = warp_row_stats<kChunks>(v, lane, a.D, a.d_true);
-    for (int k0 = b; k0 < e; k0 += 32) {
-      if (k0 != b) pos = k0 + lane < e ? sp[k0 + lane] : 0;
-      const int cnt = min(32, e - k0);
-      for (int j = 0; j < cnt; ++j)
-        assemble_row_st<kChunks>(a.o, is_hist, row_of(__shfl_sync(0xffffffffu, pos, j)), v, lane, a.D,
-                                 a.d_true, st);
-    }
+    for (int j = 0; j < e - b; ++j)
+      assemble_row_st<kChunks>(a.o, is_hist, row_of(__shfl_sync(0xffffffffu, pos, j)), v, lane, a.D, a.d_true,
+                               st);
     continue;
   }
   // zero the padding rows of this list's region (rows past the actual length)
-  const int k = u - nu;
+  const int k = u - nw;
   float4 z[kChunks];
 #pragma unroll
   for (int q = 0; q < kChunks; ++q) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
