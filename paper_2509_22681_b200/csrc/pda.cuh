@@ -6,14 +6,15 @@
 //     return table[inverse]
 // called once for the history ids and once for the candidate ids of a request.
 //
-// pda_dedup   : one CTA per id list.  Bitonic sort of (id, position) pairs in
-//               shared memory, adjacent-difference flags, block scan -> the
-//               ascending unique ids, the int64 inverse map (bit-exact with
-//               np.unique), the sorted positions and each unique id's run start.
-// pda_gather  : grid-wide.  One warp per unique id reads its embedding row ONCE
-//               (float4 / 8-byte vector loads) and writes it to every position
-//               of its run — history rows straight into the block-major row
-//               space the projection GEMMs read (Climber split, forward.py:50-62),
+// pda_dedup   : one CTA per id list.  Stable radix sort of (id, position) pairs,
+//               adjacent-difference flags, block scan -> the ascending unique ids
+//               and the int64 inverse map (bit-exact with np.unique), the sorted
+//               positions, each unique id's run start, and the gather work list
+//               (runs cut into pieces of <= kRunPiece positions).
+// pda_gather  : grid-wide.  One warp per work piece reads the id's embedding row
+//               (float4 / 8-byte vector loads) and writes it to the piece's
+//               positions — history rows straight into the block-major row space
+//               the projection GEMMs read (Climber split, forward.py:50-62),
 //               candidate rows into the shared candidate row space.
 #pragma once
 #include <cuda_bf16.h>
@@ -23,7 +24,6 @@
 
 namespace flame {
 
-constexpr int kPdaThreads = 1024;
 constexpr int kRunPiece = 32;  // positions one gather warp writes per work item
 constexpr int kPdaMaxList = 8192;  // ids per list handled by one CTA (cfg5: 8184)
 
@@ -46,10 +46,6 @@ struct PdaLists {
   int cap;             // max(H_bkt, C_bkt)
   const int* active;   // [1] requests in use (null: all R); lists of unused slots are skipped
 };
-
-__device__ __forceinline__ bool pair_less(long long ka, int pa, long long kb, int pb) {
-  return ka < kb || (ka == kb && pa < pb);
-}
 
 // Sort phase: cub::BlockRadixSort of (id, position) pairs, kThreads x kItems =
 // the list capacity.  Radix sort is stable, so equal ids keep ascending positions
