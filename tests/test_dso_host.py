@@ -103,3 +103,25 @@ def test_candidate_buckets():
     for c in range(1, 2049):
         b = cand_bucket(c)
         assert b >= c and (b < 128 or b % 128 == 0)
+
+
+def test_vectorised_plan_matches_scalar_buckets():
+    """The vectorised plan (large batches) groups exactly like bucket_of."""
+    from paper_2509_22681_b200.orchestrator import BucketScheduler
+
+    cfg = fb.ModelConfig(256, 64, 4, 1, 1024, 2, 1024, 2048)
+
+    class Eng:
+        config = cfg
+
+    sched = BucketScheduler.__new__(BucketScheduler)
+    sched.engine, sched.target_rows, sched.max_slots = Eng(), 4096, 64
+    rng = np.random.default_rng(3)
+    shapes = [(4 * int(h), int(c)) for h, c in zip(rng.integers(0, 257, 500), rng.integers(1, 2049, 500))]
+    plan = sched.plan(shapes)
+    seen = sorted(i for _, idx in plan for i in idx)
+    assert seen == list(range(500))
+    for key, idx in plan:
+        assert len(idx) <= sched.slots_for(key[1])
+        assert all(bucket_of(*shapes[i], cfg) == key for i in idx)
+        assert idx == sorted(idx)
