@@ -221,7 +221,7 @@ def run_reference(args, dist) -> None:
         return
     name = args.workload
     cores = len(os.sched_getaffinity(0))
-    procs = max(1, min(cores, 32))
+    procs = max(1, min(cores, 32, int(os.environ.get("FLAME_BENCH_CPU_PROCS", "32"))))
     per = REF_REQS_PER_PROC.get(name, 1)
     C = WORKLOADS[name][7]
     cpu = _cpu_name()
@@ -304,7 +304,7 @@ def cpu_baseline_line(args, dist, name: str):
     if dist.world_size != 1 or args.no_cpu_baseline:
         return None
     cores = len(os.sched_getaffinity(0))
-    procs = max(1, min(cores, 32))
+    procs = max(1, min(cores, 32, int(os.environ.get("FLAME_BENCH_CPU_PROCS", "32"))))
     n_req = procs * 2 * REF_REQS_PER_PROC.get(name, 1)
     r = cpu_reference_sample(name, n_req, procs, WORKLOAD_SEED + 99)
     return {"value": r["cands"] / r["busy_s"], "unit": "candidates/s", "cores": r["procs"], "kind": "port",

@@ -125,3 +125,28 @@ def test_vectorised_plan_matches_scalar_buckets():
         assert len(idx) <= sched.slots_for(key[1])
         assert all(bucket_of(*shapes[i], cfg) == key for i in idx)
         assert idx == sorted(idx)
+
+
+def test_bench_reference_arm_under_torchrun_gloo(tmp_path):
+    """The driver's launch of the reference arm at N = 2 (torchrun, one process per
+    rank): rank 0 alone times the CPU reference and prints one JSON line with the
+    reference-arm keys, the other rank exits 0."""
+    import json
+    import subprocess
+    import sys
+
+    env = dict(os.environ, FLAME_BENCH_CPU_PROCS="2", OMP_NUM_THREADS="1")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl", "reference",
+           "--gpus", "2", "--workload", "cfg1", "--steps", "1", "--warmup", "3"]
+    out = subprocess.run(cmd, cwd=str(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))), env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
