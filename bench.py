@@ -56,6 +56,9 @@ WORKLOADS = {
              "production shape: 8 blocks d=512, user seq 2048, 512 candidates/request"),
     "cfg4": (256, 64, 4, 1, 1024, 2, 1024, 2048, 256,
              "DSO: Climber ranker d=256 4 blocks, user seq 1024, Zipf candidate counts 16-2048 per request"),
+    "cfg3_l2": (512, 64, 8, 2, 2048, 2, 2048, 512, 64,
+                "SURVEY 8 sensitivity row: cfg3 with 2 layers per block (non-final layer: causal history "
+                "attention + full-row Q/K/V, O-proj, FFN)"),
     "cfg5": (768, 64, 12, 1, 3072, 2, 8184, 1024, 8,
              "long-history stress: 12 blocks d=768, user seq 8184 (=12x682), 1024 candidates"),
 }
@@ -213,7 +216,7 @@ def nearest_rank(series, p):
 
 
 # ------------------------------------------------------------------- main
-REF_REQS_PER_PROC = {"cfg1": 32, "cfg2": 2, "cfg3": 1, "cfg4": 2, "cfg5": 1}
+REF_REQS_PER_PROC = {"cfg1": 32, "cfg2": 2, "cfg3": 1, "cfg3_l2": 1, "cfg4": 2, "cfg5": 1}
 
 
 def run_reference(args, dist) -> None:
