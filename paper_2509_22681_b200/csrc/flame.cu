@@ -346,27 +346,14 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
     if (!need(d)) return fail(1, "weights too short (gate_bias)");
     for (int i = 0; i < d; ++i) gate_b[static_cast<size_t>(b) * D + i] = static_cast<float>(a[i]);
   }
-  // expert W1: bf16 mode stores the 3-term split [W_hi | W_lo | W_hi] along K
-  // (the expert head dominates the bf16 error budget: DESIGN.md §5)
-  constexpr bool kSplit = std::is_same<T, __nv_bfloat16>::value;
-  const int DK = kSplit ? 3 * D : D;
-  std::vector<T> we1(static_cast<size_t>(F) * DK, cvt<T>(0.0));
+  // expert W1: fp32 in both modes, transposed [F][D] (K-major).  The bf16 mode
+  // multiplies it as tf32 (the expert head dominates the bf16 error budget:
+  // DESIGN.md §4; plain bf16 would give 1.7e-2 at cfg5, tf32 gives 4e-3)
+  constexpr bool kSplit = std::is_same<T, __nv_bfloat16>::value;  // (bf16 mode: 2 GELU epilogue)
+  std::vector<float> we1(static_cast<size_t>(F) * D, 0.f);
   std::vector<float> be1(F, 0.f), we2(static_cast<size_t>(F) * tasks, 0.f), be2(tasks, 0.f);
   if (!need(static_cast<long long>(d) * f)) return fail(1, "weights too short (expert_w1)");
-  if (kSplit) {
-    for (int k = 0; k < d; ++k)
-      for (int n = 0; n < f; ++n) {
-        const double w = a[static_cast<size_t>(k) * f + n];
-        const __nv_bfloat16 hi = __float2bfloat16_rn(static_cast<float>(w));
-        const __nv_bfloat16 lo = __float2bfloat16_rn(static_cast<float>(w - static_cast<double>(__bfloat162float(hi))));
-        T* row = we1.data() + static_cast<size_t>(n) * DK;
-        row[k] = cvt<T>(__bfloat162float(hi));
-        row[D + k] = cvt<T>(__bfloat162float(lo));
-        row[2 * D + k] = cvt<T>(__bfloat162float(hi));
-      }
-  } else {
-    pack_transposed(we1, 0, F, D, a, d, f, id_f, id_d);
-  }
+  pack_transposed(we1, 0, F, D, a, d, f, id_f, id_d);
   if (!need(f)) return fail(1, "weights too short (expert_b1)");
   for (int i = 0; i < f; ++i) be1[i] = static_cast<float>(a[i]);
   if (!need(static_cast<long long>(f) * tasks)) return fail(1, "weights too short (expert_w2)");
@@ -400,7 +387,7 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
       return fail(2, "device allocation / copy of layer weights failed");
     lw.wqkv = wqkv; lw.wo = wo; lw.w1 = w1; lw.w2 = w2;
   }
-  T* we1d;
+  float* we1d;
   if (!up(gate_w, &c->gate_w) || !up(gate_b, &c->gate_b) || !up(we1, &we1d) || !up(be1, &c->be1) ||
       !up(we2, &c->we2) || !up(we2p, &c->we2p) || !up(be2, &c->be2) || !up(scale, &c->scale) ||
       !up(scale_log2, &c->scale_log2))
@@ -446,7 +433,7 @@ struct Pipe {
   Prof* prof = nullptr;
 
   Act* act(void* p) { return static_cast<Act*>(p); }
-  static constexpr int kSplitK = std::is_same<Act, __nv_bfloat16>::value ? 3 : 1;
+  static constexpr int kSplitK = 1;  // the fused operand is one fp32 row (tf32 expert GEMM)
 
   void mark(const char* name, double flops, double bytes) {
     if (!prof) return;
@@ -821,7 +808,7 @@ struct Pipe {
         resid_b = reinterpret_cast<const __nv_bfloat16*>(Y) + r0 * D;
         gate_w = c->gate_w; gate_b = c->gate_b;
         if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F,
-                          G, e->Fz, kSplitK * D, 0, 0, w.b2, D, nullptr, D, gD,
+                          G, e->Fz, D, 0, 0, w.b2, D, nullptr, D, gD,
                           EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_GATED)) return rc;
         gated_done = true;
       } else if constexpr (kFold) {
@@ -839,20 +826,20 @@ struct Pipe {
     // gated fusion over blocks (forward.py:143-156)
     if (!gated_done) {
       const long long n = Rc * (D / 4);
-      mark("gated_fusion", 0.0, static_cast<double>(Rc) * D * (4.0 * G + kSplitK * sizeof(Act)));
-      gated_fusion_rows<Act><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-          Xcur + Rh * D, D, gD, G, c->gate_w, c->gate_b, act(e->Fz), kSplitK * D, static_cast<int>(Rc), D);
+      mark("gated_fusion", 0.0, static_cast<double>(Rc) * D * (4.0 * G + 4.0));
+      gated_fusion_rows<float><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+          Xcur + Rh * D, D, gD, G, c->gate_w, c->gate_b, static_cast<float*>(e->Fz), D, static_cast<int>(Rc), D);
       if (int rc = check()) return rc;
     }
     // expert heads (forward.py:159-166)
     gemm_name = "gemm_expert_w1";
     if (kFold && c->tasks <= 4) {
-      // split-bf16 K = 3D over [Fz_hi|Fz_hi|Fz_lo] x [W_hi|W_lo|W_hi]; the epilogue applies
+      // fp32 fused rows x fp32 W_e1, multiplied as tf32 (kind::tf32); the epilogue applies
       // bias + GELU and dots each row with expert_w2, so the hidden layer never reaches HBM
-      dot_w = c->we2p; dot_n = c->tasks; flop_div = 3.0;
-      if (int rc = gemm(act(e->Fz), kSplitK * D, 0, 1, act(c->we1), kSplitK * D, 0, static_cast<int>(Rc), F,
-                        kSplitK * D, 1, e->partial, 0, 0, 0, c->be1, 0, nullptr, 0, 0,
-                        EPI_BIAS | EPI_GELU | EPI_ROWDOT)) return rc;
+      dot_w = c->we2p; dot_n = c->tasks;
+      if (int rc = gemm(reinterpret_cast<const Act*>(e->Fz), D, 0, 1, reinterpret_cast<const Act*>(c->we1), D, 0,
+                        static_cast<int>(Rc), F, D, 1, e->partial, 0, 0, 0, c->be1, 0, nullptr, 0, 0,
+                        EPI_BIAS | EPI_GELU | EPI_ROWDOT | (kFold ? EPI_TF32 : 0))) return rc;
       const int n_parts = gemm_row_parts(F, EPI_BIAS | EPI_GELU | EPI_ROWDOT);
       mark("expert_combine", 0.0, static_cast<double>(Rc) * n_parts * c->tasks * 4.0);
       expert_combine<<<static_cast<unsigned>((Rc + 255) / 256), 256, 0, s>>>(
@@ -860,9 +847,9 @@ struct Pipe {
           static_cast<int>(Rc));
       if (int rc = check()) return rc;
     } else {
-      flop_div = kSplitK;
-      if (int rc = gemm(act(e->Fz), kSplitK * D, 0, 1, act(c->we1), kSplitK * D, 0, static_cast<int>(Rc), F,
-                        kSplitK * D, 1, e->He, F, 0, 0, c->be1, 0, nullptr, 0, 0, EPI_BIAS | EPI_GELU | EPI_OUT_F32))
+      if (int rc = gemm(reinterpret_cast<const Act*>(e->Fz), D, 0, 1, reinterpret_cast<const Act*>(c->we1), D, 0,
+                        static_cast<int>(Rc), F, D, 1, e->He, F, 0, 0, c->be1, 0, nullptr, 0, 0,
+                        EPI_BIAS | EPI_GELU | EPI_OUT_F32 | (kFold ? EPI_TF32 : 0)))
         return rc;
       const long long threads = Rc * 32;
       mark("expert_out", 2.0 * Rc * F * c->tasks, static_cast<double>(Rc) * F * 4.0);
@@ -1103,7 +1090,7 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
   e->Hf = A(G * rows * F * ab);
   e->Xa = static_cast<float*>(A(G * rows * D * 4));
   e->Xb = c->L > 1 ? static_cast<float*>(A(G * rows * D * 4)) : nullptr;
-  e->Fz = A(e->Rc * D * ab * (fold ? 3 : 1));
+  e->Fz = A(e->Rc * D * 4);  // fp32 fused rows (both modes)
   e->He = (fold && c->tasks <= 4) ? nullptr : A(e->Rc * F * 4);
   e->spos = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
   e->ustart = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));

@@ -9,11 +9,12 @@
 namespace flame {
 
 struct GemmProblem {
-  // A: bf16 [G or 1][M][lda], K-major; W: bf16 [G][N][ldw] (transposed weight)
-  const __nv_bfloat16* A;
+  // A: bf16 (fp32 with EPI_TF32) [G or 1][M][lda], K-major; W: same type [G][N][ldw]
+  // (transposed weight)
+  const void* A;
   long long lda, a_gstride;
   int a_shared;  // 1: every group reads the same A
-  const __nv_bfloat16* W;
+  const void* W;
   long long ldw, w_gstride;
   int M, N, K, G;
   GemmEpilogue ep;
@@ -74,9 +75,13 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   const int ncl = (gemm_cluster_pref() == 2 && m_tiles >= 2 && max_clusters > 0 && p.K >= pair_min_k) ? 2 : 1;
   CUtensorMap ta, tb;
   const int ga = p.a_shared ? 1 : p.G;
-  if (!make_tmap_bf16_3d(&ta, p.A, p.K, p.M, ga, p.lda * 2, p.a_gstride * 2, gemm::BK, gemm::BM))
+  constexpr bool kTF32 = (EPI & EPI_TF32) != 0;
+  constexpr int kEs = kTF32 ? 4 : 2;                     // operand element bytes
+  constexpr int kBKe = kTF32 ? 32 : gemm::BK;            // K elements per 128-byte row
+  auto in_map = kTF32 ? make_tmap_f32_3d : make_tmap_bf16_3d;
+  if (!in_map(&ta, p.A, p.K, p.M, ga, p.lda * kEs, p.a_gstride * kEs, kBKe, gemm::BM))
     return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_3d(&tb, p.W, p.K, p.N, p.G, p.ldw * 2, p.w_gstride * 2, gemm::BK, BN / ncl))
+  if (!in_map(&tb, p.W, p.K, p.N, p.G, p.ldw * kEs, p.w_gstride * kEs, kBKe, BN / ncl))
     return cudaErrorInvalidValue;
   CUtensorMap to;
   constexpr int ob = (EPI & EPI_OUT_F32) ? 4 : 2;
@@ -84,8 +89,8 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
     // row-dot epilogue writes its partials directly; the map is a valid placeholder
     if (!make_tmap_out_3d(&to, p.ep.out, 4, 32, p.M, 1, 128, 0)) return cudaErrorInvalidValue;
   } else if constexpr (C::kGated) {
-    // one [M][3N] bf16 output (hi | hi | lo) shared by all groups
-    if (!make_tmap_out_3d(&to, p.ep.out, 2, 3ull * p.N, p.M, 1, p.ep.out_ld * 2, 0)) return cudaErrorInvalidValue;
+    // one [M][N] fp32 output (the gated sum) shared by all groups
+    if (!make_tmap_out_3d(&to, p.ep.out, 4, p.N, p.M, 1, p.ep.out_ld * 4, 0)) return cudaErrorInvalidValue;
   } else if (!make_tmap_out_3d(&to, p.ep.out, ob, static_cast<uint64_t>(p.ep.out_col0) + p.N, p.M, p.G,
                                p.ep.out_ld * ob, p.ep.out_gstride * ob)) {
     return cudaErrorInvalidValue;
@@ -110,7 +115,7 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
     const int total = p.G * m_tiles * n_tiles;
     const int grid = total < num_sms ? total : num_sms;
     gemm_bf16_tcgen05<BN, EPI, 1><<<grid, C1::kThreads, C1::kSmemBytes, s>>>(
-        ta, tb, to, to2, tr, p.K / gemm::BK, m_tiles, n_tiles, p.G, p.a_shared, ep);
+        ta, tb, to, to2, tr, p.K / kBKe, m_tiles, n_tiles, p.G, p.a_shared, ep);
     return cudaGetLastError();
   }
   const int total_pairs = p.G * ((m_tiles + 1) / 2) * n_tiles;
@@ -127,7 +132,7 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   q.stream = s;
   q.attrs = at;
   q.numAttrs = 1;
-  return cudaLaunchKernelEx(&q, gemm_bf16_tcgen05<BN, EPI, 2>, ta, tb, to, to2, tr, p.K / gemm::BK, m_tiles, n_tiles,
+  return cudaLaunchKernelEx(&q, gemm_bf16_tcgen05<BN, EPI, 2>, ta, tb, to, to2, tr, p.K / kBKe, m_tiles, n_tiles,
                             p.G, p.a_shared, ep);
 }
 
@@ -155,6 +160,10 @@ static cudaError_t launch_gemm_bn(const GemmProblem& p, cudaStream_t s, int num_
       return launch_gemm_t<BN, EPI_LNSTATS | EPI_BIAS | EPI_GELU>(p, s, num_sms);
     case EPI_BIAS | EPI_GELU | EPI_ROWDOT:
       return launch_gemm_t<BN, EPI_BIAS | EPI_GELU | EPI_ROWDOT>(p, s, num_sms);
+    case EPI_BIAS | EPI_GELU | EPI_ROWDOT | EPI_TF32:
+      return launch_gemm_t<BN, EPI_BIAS | EPI_GELU | EPI_ROWDOT | EPI_TF32>(p, s, num_sms);
+    case EPI_BIAS | EPI_GELU | EPI_OUT_F32 | EPI_TF32:
+      return launch_gemm_t<BN, EPI_BIAS | EPI_GELU | EPI_OUT_F32 | EPI_TF32>(p, s, num_sms);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -171,7 +180,7 @@ static unsigned long long* g_gemm_trace_buf = nullptr;
 static int g_gemm_trace_which = -1, g_gemm_trace_count = 0;
 
 static cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t s, int num_sms) {
-  if (p.K % gemm::BK != 0 || p.M < 1 || p.N < 1 || p.G < 1) return cudaErrorInvalidValue;
+  if (p.K % ((p.epi & EPI_TF32) ? 32 : gemm::BK) != 0 || p.M < 1 || p.N < 1 || p.G < 1) return cudaErrorInvalidValue;
   if (g_gemm_trace_buf != nullptr) {
     unsigned long long* v = g_gemm_trace_count++ == g_gemm_trace_which ? g_gemm_trace_buf : nullptr;
     cudaError_t e = cudaMemcpyToSymbolAsync(g_gemm_trace, &v, sizeof(v), 0, cudaMemcpyHostToDevice, s);

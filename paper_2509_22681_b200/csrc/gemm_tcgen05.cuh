@@ -65,7 +65,7 @@ struct GemmEpilogue {
   // EPI_GATED (FFN W2 of the last layer + gated fusion): per group g the tile's
   // X2 = acc + b2 + X1 is folded into sum_g sigmoid(X2 * gate_w[g] + gate_b[g]) * X2
   // (kept in TMEM across the groups, which one CTA walks in order); only the sum
-  // reaches HBM, as the split-bf16 [hi | hi | lo] expert operand ([M][3N] bf16)
+  // reaches HBM, as the fp32 operand of the tf32 expert GEMM ([M][N])
   const float* gate_w;    // [G][N]
   const float* gate_b;    // [G][N]
   // device-side active row count (DSO executors): rows >= *m_active * rows_per_slot
@@ -91,6 +91,7 @@ enum : int {
   EPI_LNSTATS = 128,
   EPI_RESID_BF16 = 256,
   EPI_GATED = 512,
+  EPI_TF32 = 2048,  // operands are fp32, multiplied as tf32 (kind::tf32): 32 K-elements per 128-byte row
 };
 
 // Debug-only event trace of CTA 0 (flame_debug_gemm_trace): slot 0 = MMA issuer,
@@ -143,7 +144,7 @@ struct Cfg {
                 "gated-fusion epilogue: BN = 128, bf16 output, bf16 residual");
   // STATS with an fp32 primary output, and the gated sum (hi + lo halves), also
   // stage a second bf16 box
-  static constexpr bool kDual = ((EPI & EPI_STATS) != 0 && kF32) || kGated;
+  static constexpr bool kDual = (EPI & EPI_STATS) != 0 && kF32;
   // staging slots per epilogue warp ([out box | bf16 side box]); with two, a
   // chunk's staging does not wait for the previous chunk's TMA store to read smem.
   // Measured at cfg3: pays for the GELU (FFN W1) epilogue (0.533 -> 0.497 ms),
@@ -152,7 +153,8 @@ struct Cfg {
   static constexpr int kOutBoxes =
       FLAME_GEMM_OUT_BOXES != 0 ? (FLAME_GEMM_OUT_BOXES == 2 && !kF32 ? 2 : 1)
                                 : ((EPI & EPI_GELU) != 0 && !kF32 && !kRowDot ? 2 : 1);
-  static constexpr int kOutBoxBytes = kRowDot ? 0 : 32 * 32 * (kF32 ? 4 : 2);
+  // (the gated-fusion sum leaves as fp32: the tf32 expert GEMM reads it)
+  static constexpr int kOutBoxBytes = kRowDot ? 0 : 32 * 32 * ((kF32 || kGated) ? 4 : 2);
   static constexpr int kSlotBytes = kOutBoxBytes + (kDual ? 32 * 32 * 2 : 0);
   static constexpr int kBoxBytes = kOutBoxes * kSlotBytes;
   // chunks of 32 columns per warp and the per-warp column-vector slices
@@ -189,6 +191,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
                       const __grid_constant__ CUtensorMap tmR, int num_k_blocks, int m_tiles_max, int n_tiles, int groups, int a_shared, GemmEpilogue ep) {
   using C = gemm::Cfg<BN, EPI, kCG>;
   constexpr int kEpiWarps = C::kEpiWarps;
+  constexpr bool kTF32 = (EPI & EPI_TF32) != 0;
+  constexpr int kBKe = kTF32 ? 32 : gemm::BK;  // K elements per 128-byte smem row
   constexpr int kEpiPerQuad = kEpiWarps / 4;
   constexpr int kStages = C::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -296,17 +300,17 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
 #endif
           if constexpr (kCG == 1) {
             ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-            ptx::tma_load_3d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * gemm::BK,
+            ptx::tma_load_3d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * kBKe,
                              m_blk * gemm::BM, ga);
-            ptx::tma_load_3d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * gemm::BK,
+            ptx::tma_load_3d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * kBKe,
                              n_blk * BN, g);
           } else {
             // this CTA's A rows and its half of the W tile, both completing on the
             // even CTA's full barrier (which expects the pair's bytes)
             if (crank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
             const uint32_t fb = ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0);
-            ptx::tma_load_3d_cg2(smem_a + stage * C::kABytes, &tmA, fb, kb * gemm::BK, m_blk * gemm::BM, ga);
-            ptx::tma_load_3d_cg2(smem_b + stage * C::kBBytes, &tmB, fb, kb * gemm::BK,
+            ptx::tma_load_3d_cg2(smem_a + stage * C::kABytes, &tmA, fb, kb * kBKe, m_blk * gemm::BM, ga);
+            ptx::tma_load_3d_cg2(smem_b + stage * C::kBBytes, &tmB, fb, kb * kBKe,
                                  n_blk * BN + crank * (BN / 2), g);
           }
         }
@@ -325,7 +329,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   } else if (warp == 1 && crank == 0) {
     // --------------------------------------------------------- MMA issuer
     const bool leader = ptx::elect_one();
-    constexpr uint32_t idesc = ptx::make_idesc_bf16(gemm::BM * kCG, BN, 0, 0);
+    constexpr uint32_t idesc = kTF32 ? ptx::make_idesc_tf32(gemm::BM * kCG, BN)
+                                     : ptx::make_idesc_bf16(gemm::BM * kCG, BN, 0, 0);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -347,8 +352,14 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
           for (int k = 0; k < gemm::BK / 16; ++k) {
             const uint64_t ad = ptx::make_desc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = ptx::make_desc_sw128(b_addr + k * 32, 16, 1024);
-            if constexpr (kCG == 1) ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            else ptx::mma_bf16_ss_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            // four 32-byte K steps per 128-byte row: K = 16 bf16 or 8 tf32 each
+            if constexpr (kTF32) {
+              if constexpr (kCG == 1) ptx::mma_tf32_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              else ptx::mma_tf32_ss_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            } else {
+              if constexpr (kCG == 1) ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              else ptx::mma_bf16_ss_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
           }
           if constexpr (kCG == 1) ptx::mma_commit(&empty[stage]);
           else ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
@@ -665,16 +676,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
           uint8_t* box2 = ob + C::kOutBoxBytes;  // bf16 side-output box (kDual)
           if constexpr (C::kOutBoxes > 1) box_i ^= 1;
           if constexpr (C::kGated) {
-            // split-bf16 expert operand: hi = bf16(sum), lo = bf16(sum - hi)
-            float lo[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float hi = __bfloat162float(__float2bfloat16_rn(v[j]));
-              lo[j] = v[j] - hi;
-              v[j] = hi;
-            }
-            stage_row32<false>(ob, lane, v);
-            stage_row32<false>(box2, lane, lo);
+            stage_row32<true>(ob, lane, v);  // the fp32 gated sum (tf32 expert operand)
           } else {
             stage_row32<kF32>(ob, lane, v);
             if constexpr (C::kDual) stage_row32<false>(box2, lane, v);
@@ -684,10 +686,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
           if (epi_leader) {
             if (row0 < ep.M) {
               if constexpr (C::kGated) {
-                // [hi | hi | lo], one group of 3N columns
-                ptx::tma_store_3d(&tmO, ob, col0, row0, 0);
-                ptx::tma_store_3d(&tmO, ob, ep.N + col0, row0, 0);
-                ptx::tma_store_3d(&tmO, box2, 2 * ep.N + col0, row0, 0);
+                ptx::tma_store_3d(&tmO, ob, col0, row0, 0);  // one [M][N] fp32 output for all groups
               } else {
                 ptx::tma_store_3d(&tmO, ob, ep.out_col0 + col0, row0, g);
                 if constexpr (C::kDual) ptx::tma_store_3d(&tmO2, box2, col0, row0, g);

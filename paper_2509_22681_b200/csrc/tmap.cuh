@@ -44,6 +44,26 @@ inline bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t inner
   return r == CUDA_SUCCESS;
 }
 
+// Same for fp32 operands (the tf32 GEMM): box_inner * 4 <= 128.
+inline bool make_tmap_f32_3d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows, uint64_t groups,
+                             uint64_t row_stride_bytes, uint64_t group_stride_bytes, uint32_t box_inner,
+                             uint32_t box_rows) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  std::memset(map, 0, sizeof(*map));
+  if (groups < 1) groups = 1;
+  if (group_stride_bytes == 0) group_stride_bytes = rows * row_stride_bytes;
+  if (group_stride_bytes == 0) group_stride_bytes = 16;
+  cuuint64_t dims[3] = {inner, rows, groups};
+  cuuint64_t strides[2] = {row_stride_bytes, group_stride_bytes};
+  cuuint32_t box[3] = {box_inner, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Output map for the GEMM epilogue's TMA stores: [groups][rows][cols] of
 // bf16 (2-byte) or fp32 (4-byte) elements, box 32 cols x 32 rows; swizzle
 // matches a 32-column row (64 B -> SW64, 128 B -> SW128).
