@@ -178,7 +178,10 @@ struct Cfg {
   static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
   static_assert(kStages >= 2, "GEMM smem ring too shallow");
   // two accumulators (+ the gated running sum at columns [2 BN, 3 BN))
-  static constexpr int kTmemCols = kGated ? 512 : 2 * BN;
+  // accumulator ring: as many BN-column buffers as TMEM holds (BN = 128: four), so
+  // the MMAs can run several tiles ahead of a latency-bound epilogue
+  static constexpr int kAcc = kGated ? 2 : 512 / BN;
+  static constexpr int kTmemCols = kGated ? 512 : kAcc * BN;
   static constexpr int kSmemBytes = kStages * kStageBytes + kFixed;
 };
 
@@ -207,10 +210,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_resid + kEpiWarps * C::kResidBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
-  uint64_t* tmem_full = bars + 2 * kStages;
-  uint64_t* tmem_empty = bars + 2 * kStages + 2;
-  uint64_t* resid_full = bars + 2 * kStages + 4;  // [kEpiWarps][2]
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4 + 2 * kEpiWarps);
+  uint64_t* tmem_full = bars + 2 * kStages;               // [kAcc]
+  uint64_t* tmem_empty = tmem_full + C::kAcc;             // [kAcc]
+  uint64_t* resid_full = tmem_empty + C::kAcc;            // [kEpiWarps][2]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(resid_full + 2 * kEpiWarps);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::kAcc; ++s) {
       ptx::mbar_init(&tmem_full[s], 1);
       ptx::mbar_init(&tmem_empty[s], kEpiWarps * kCG);  // both CTAs' epilogue warps
     }
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       }
       __syncwarp();
       GEMM_TRACE(0, 3);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::kAcc) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
     // ----------------------------------------------------------- epilogue
@@ -754,7 +757,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         else ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tmem_empty[acc]), 0));
       }
       EPI_TRACE(6);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::kAcc) { acc = 0; acc_phase ^= 1; }
     }
     if (epi_leader) ptx::tma_store_wait<0>();
     __syncwarp();
