@@ -5,7 +5,7 @@ O=gpurun_out/measure; mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo pytest=$? >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke=$? >> $O/smoke.log
 timeout 600 python tools/parity_report.py --json $O/parity.json > $O/parity.log 2>&1
-for w in cfg3 cfg4 cfg2 cfg5 cfg1; do
+for w in cfg3 cfg4 cfg2 cfg5 cfg1 cfg3_l2; do
   timeout 900 python bench.py --workload $w --steps 20 --warmup 5 > $O/bench_$w.log 2>&1
   tail -1 $O/bench_$w.log > $O/bench_$w.json
 done

@@ -76,5 +76,19 @@ How to read the table:
 
 """ + f"fp32 verification mode: at most {max(p['maxabs_fp32'] for p in par):.1e} (tolerance 1e-4).\n" + \
     f"bf16: at most {max(p['maxabs_bf16'] for p in par):.1e} (tolerance 2e-2).\n"
+l2 = P / "bench_cfg3_l2.json"
+if l2.exists():
+    d = json.loads(l2.read_text())
+    s += f"""
+## Sensitivity row: cfg3 with 2 layers per block (`bench_cfg3_l2.json`)
+
+SURVEY §8 asks for `L = 2` beside the L = 1 reading. Layer 1 of each block is a
+non-final layer: Q/K/V on all rows, causal history attention, O-proj and FFN on
+all rows, with an fp32 residual stream. This row measures that path at full size:
+
+* {d['value'] / 1e6:.2f} M cand/s device ({d['ms_per_step']:.2f} ms/step);
+* {d['e2e']['value'] / 1e6:.2f} M e2e;
+* {d['step_tflops']:.0f} TFLOP/s algorithmic.
+"""
 (P / "SUMMARY.md").write_text(s)
 print(s[:1500])
