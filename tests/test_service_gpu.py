@@ -106,3 +106,44 @@ def test_refresh_from_store_wire_values(gpu):
     want = orc.model_forward(hist, cand, svc.params, CFG)
     assert np.abs(got - want).max() <= 2e-2
     svc.close()
+
+
+def test_concurrent_handle_request_threads(gpu):
+    """Requests from several threads (the reference service is thread-safe,
+    service.py:127-171) score exactly as when issued one by one."""
+    import threading
+
+    svc = DeviceService(CFG, num_items=NUM_ITEMS, target_rows=256)
+    rng = np.random.default_rng(12)
+    reqs = [request_of(rng.integers(0, NUM_ITEMS, 2 * int(rng.integers(0, 33))), rng.integers(0, NUM_ITEMS, int(c)))
+            for c in rng.integers(1, 33, 16)]
+    want = [svc.handle_request(r).scores for r in reqs]
+    got = [None] * len(reqs)
+
+    def worker(k):
+        for i in range(k, len(reqs), 4):
+            got[i] = svc.handle_request(reqs[i]).scores
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for g, w in zip(got, want):
+        np.testing.assert_array_equal(g, w)
+    svc.close()
+
+
+def test_bf16_table_refresh(gpu):
+    """A bf16 device table takes the same row / value refreshes (rounded to bf16)."""
+    svc = DeviceService(CFG, num_items=NUM_ITEMS, target_rows=256, table_dtype="bf16")
+    req = request_of(range(8), [5, 6])
+    base = svc.handle_request(req).scores
+    svc.mutate([5])
+    svc.refresh_values([6], [b""])
+    after = svc.handle_request(req).scores
+    assert not np.array_equal(base, after)
+    cand = np.stack([svc.embedding_of(5), np.zeros(CFG.hidden_dim)])
+    want = orc.model_forward(resolve(req.history_item_ids), cand, svc.params, CFG)
+    assert np.abs(after - want).max() <= 2e-2
+    svc.close()
