@@ -95,6 +95,7 @@ struct LayerW {
   float* cqkv = nullptr;  // [G][3DA]
   float* c1 = nullptr;    // [G][F]
   float* u1 = nullptr;    // [G][F] ln2_scale @ w1 (mean correction of the folded LN2)
+  float* uqkv = nullptr;  // [G][3DA] ln1_scale @ w_qkv (mean correction of the folded LN1, layers > 0)
 };
 
 }  // namespace
@@ -142,6 +143,7 @@ struct FlameExec {
   float* Eh = nullptr;
   float* Ec = nullptr;
   void* Y = nullptr;
+  void* Y2 = nullptr;  // bf16 copy of a non-final layer's output (the next layer's LN1 input), L >= 2
   void* QKV = nullptr;
   void* AO = nullptr;
   float* X1 = nullptr;
@@ -254,13 +256,14 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
   constexpr bool kFold = std::is_same<T, __nv_bfloat16>::value;  // bf16 path folds LayerNorm
   struct HostLayer {
     std::vector<T> wqkv, wo, w1, w2;
-    std::vector<float> b1, b2, l1g, l1b, l2g, l2b, cqkv, c1, u1;
+    std::vector<float> b1, b2, l1g, l1b, l2g, l2b, cqkv, c1, u1, uqkv;
   };
   std::vector<HostLayer> hl(L);
   for (auto& h : hl) {
     h.cqkv.assign(static_cast<size_t>(G) * 3 * DA, 0.f);
     h.c1.assign(static_cast<size_t>(G) * F, 0.f);
     h.u1.assign(static_cast<size_t>(G) * F, 0.f);
+    h.uqkv.assign(static_cast<size_t>(G) * 3 * DA, 0.f);
     h.wqkv.assign(static_cast<size_t>(G) * 3 * DA * D, cvt<T>(0.0));
     h.wo.assign(static_cast<size_t>(G) * D * DA, cvt<T>(0.0));
     h.w1.assign(static_cast<size_t>(G) * F * D, cvt<T>(0.0));
@@ -308,7 +311,8 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
       for (int q = 0; q < 3; ++q) {
         if (kFold)
           pack_transposed_folded(h.wqkv, qkv_off, D, wsrc[q], d, d, *maps[q], id_d, lnsrc[0], lnsrc[1],
-                                 h.cqkv.data() + static_cast<size_t>(b) * 3 * DA);
+                                 h.cqkv.data() + static_cast<size_t>(b) * 3 * DA,
+                                 h.uqkv.data() + static_cast<size_t>(b) * 3 * DA);
         else
           pack_transposed(h.wqkv, qkv_off, 3 * DA, D, wsrc[q], d, d, *maps[q], id_d);
       }
@@ -383,7 +387,7 @@ int upload_weights(FlameCtx* c, const double* w, long long n_values) {
     if (!up(h.wqkv, &wqkv) || !up(h.wo, &wo) || !up(h.w1, &w1) || !up(h.w2, &w2) ||
         !up(h.b1, &lw.b1) || !up(h.b2, &lw.b2) || !up(h.l1g, &lw.ln1_g) || !up(h.l1b, &lw.ln1_b) ||
         !up(h.l2g, &lw.ln2_g) || !up(h.l2b, &lw.ln2_b) || !up(h.cqkv, &lw.cqkv) || !up(h.c1, &lw.c1) ||
-        !up(h.u1, &lw.u1))
+        !up(h.u1, &lw.u1) || !up(h.uqkv, &lw.uqkv))
       return fail(2, "device allocation / copy of layer weights failed");
     lw.wqkv = wqkv; lw.wo = wo; lw.w1 = w1; lw.w2 = w2;
   }
@@ -735,31 +739,42 @@ struct Pipe {
           A_h = static_cast<const Act*>(e->Ehc); A_h_g = Rh * D; rs_h = e->rs_h; rs_h_g = Rh;
           A_c = static_cast<const Act*>(e->Ecc); A_c_g = 0; A_c_shared = 1; rs_c = e->rs_c; rs_c_g = 0;
         } else {
-          if (int rc = center(src_h, gD, Y, gD, RS, rows, Rh)) return rc;
-          if (int rc = center(src_c, gD, Y + Rh * D, gD, RS + Rh, rows, Rc)) return rc;
-          A_h = Y; A_h_g = gD; rs_h = RS; rs_h_g = rows;
-          A_c = Y + Rh * D; A_c_g = gD; rs_c = RS + Rh; rs_c_g = rows;
+          // the previous layer's W2 epilogue left a bf16 copy of its output (Y2) and
+          // per-row (sum, sumsq) partials (STATS): the QKV epilogues apply LN1 as
+          // rstd (x W' - mean u) + c, so no centering pass
+          A_h = static_cast<const Act*>(e->Y2); A_h_g = gD;
+          A_c = static_cast<const Act*>(e->Y2) + Rh * D; A_c_g = gD;
         }
       } else {
         if (int rc = layer_norm(src_h, D, src_h_g, Y, D, gD, w.ln1_g, w.ln1_b, Rh)) return rc;
         if (int rc = layer_norm(src_c, D, src_c_g, Y + Rh * D, D, gD, w.ln1_g, w.ln1_b, Rc)) return rc;
         A_h = Y; A_h_g = gD; A_c = Y + Rh * D; A_c_g = gD;
       }
-      const int qkv_epi = kFold ? (EPI_ROWSCALE | EPI_BIAS) : 0;
+      const bool ln1_stats = kFold && l > 0;
+      const int qkv_epi = kFold ? (ln1_stats ? (EPI_LNSTATS | EPI_BIAS) : (EPI_ROWSCALE | EPI_BIAS)) : 0;
+      const long long SP1 = static_cast<long long>(e->stat_parts) * 2;  // floats per row of STATS
+      auto ln1_consumer = [&](long long r0, const float* colsum) {
+        if (!ln1_stats) return;
+        ln.lnstats = e->STATS + r0 * SP1; ln.lnstats_gstride = rows * SP1; ln.stats_parts = e->stat_parts;
+        ln.d_true = c->d; ln.colsum = colsum; ln.colsum_gstride = 3LL * DA;
+      };
       // projections (forward.py:112-114 last layer: history rows K,V only; :121-123 others)
       const Act* Wqkv = act(w.wqkv);
       rs_ptr = rs_h; rs_g = rs_h_g;
       if (last) {
         gemm_name = "gemm_kv_hist";
+        ln1_consumer(0, w.uqkv + DA);
         if (int rc = gemm(A_h, D, A_h_g, 0, Wqkv + static_cast<long long>(DA) * D, D, 3LL * DA * D, Rh, 2 * DA, D, G,
                           QKV, 3LL * DA, gQKV, DA, w.cqkv + DA, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
       } else {
         gemm_name = "gemm_qkv_hist";
+        ln1_consumer(0, w.uqkv);
         if (int rc = gemm(A_h, D, A_h_g, 0, Wqkv, D, 3LL * DA * D, Rh, 3 * DA, D, G, QKV, 3LL * DA, gQKV, 0,
                           w.cqkv, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
       }
       rs_ptr = rs_c; rs_g = rs_c_g;
       gemm_name = "gemm_qkv_cand";
+      ln1_consumer(Rh, w.uqkv);
       if (int rc = gemm(A_c, D, A_c_g, A_c_shared, Wqkv, D, 3LL * DA * D, Rc, 3 * DA, D, G, QKV + Rh * 3LL * DA,
                         3LL * DA, gQKV, 0, w.cqkv, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
       // SUMI attention (attention.py:118-146; :149-178 for non-final layers)
@@ -813,9 +828,16 @@ struct Pipe {
         gated_done = true;
       } else if constexpr (kFold) {
         resid_b = reinterpret_cast<const __nv_bfloat16*>(Y) + r0 * D;
+        int w2_epi = EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32;
+        if (!last) {
+          // non-final layer: also the bf16 copy + row statistics the next layer's
+          // folded LN1 consumes (STATS layout as the O-proj's)
+          w2_epi |= EPI_STATS;
+          ln.stats = e->STATS + r0 * SP; ln.stats_gstride = rows * SP;
+          ln.out2 = static_cast<__nv_bfloat16*>(e->Y2) + r0 * D; ln.out2_ld = D; ln.out2_gstride = gD;
+        }
         if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F,
-                          G, Xnext + r0 * D, D, gD, 0, w.b2, D, nullptr, D, gD,
-                          EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32)) return rc;
+                          G, Xnext + r0 * D, D, gD, 0, w.b2, D, nullptr, D, gD, w2_epi)) return rc;
       } else {
         if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F,
                           G, Xnext + r0 * D, D, gD, 0, w.b2, D, e->X1 + r0 * D, D, gD,
@@ -1084,6 +1106,7 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
     if (c->tasks <= 4) e->partial = static_cast<float*>(A(e->Rc * n_parts * c->tasks * 4));
   }
   e->Y = A(G * rows * D * ab);
+  if (fold && c->L > 1) e->Y2 = A(G * rows * D * 2);
   e->QKV = A(G * rows * 3 * DA * ab);
   e->AO = A(G * rows * DA * ab);
   e->X1 = fold ? nullptr : static_cast<float*>(A(G * rows * D * 4));

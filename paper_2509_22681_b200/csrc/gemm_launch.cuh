@@ -156,6 +156,10 @@ static cudaError_t launch_gemm_bn(const GemmProblem& p, cudaStream_t s, int num_
     case EPI_RESID | EPI_STATS: return launch_gemm_t<BN, EPI_RESID | EPI_STATS>(p, s, num_sms);
     case EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32:
       return launch_gemm_t<BN, EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32>(p, s, num_sms);
+    case EPI_LNSTATS | EPI_BIAS:
+      return launch_gemm_t<BN, EPI_LNSTATS | EPI_BIAS>(p, s, num_sms);
+    case EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32 | EPI_STATS:
+      return launch_gemm_t<BN, EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_OUT_F32 | EPI_STATS>(p, s, num_sms);
     case EPI_LNSTATS | EPI_BIAS | EPI_GELU:
       return launch_gemm_t<BN, EPI_LNSTATS | EPI_BIAS | EPI_GELU>(p, s, num_sms);
     case EPI_BIAS | EPI_GELU | EPI_ROWDOT:
