@@ -156,7 +156,6 @@ struct FlameExec {
   void* Ecc = nullptr;         // bf16 path: centered candidate rows [Rc][D]
   float* rs_h = nullptr;       // rstd of the history rows [G][Rh]
   float* rs_c = nullptr;       // rstd of the candidate rows [Rc]
-  float* RS = nullptr;         // rstd of centered rows of later LayerNorms [G][rows]
   float* partial = nullptr;    // expert row-dot partials [Rc][n_parts][tasks]
   float* STATS = nullptr;      // folded LN2: per-row (sum, sumsq) partials [G][rows][stat_parts][2]
   int stat_parts = 0;
@@ -437,7 +436,6 @@ struct Pipe {
   Prof* prof = nullptr;
 
   Act* act(void* p) { return static_cast<Act*>(p); }
-  static constexpr int kSplitK = 1;  // the fused operand is one fp32 row (tf32 expert GEMM)
 
   void mark(const char* name, double flops, double bytes) {
     if (!prof) return;
@@ -463,7 +461,7 @@ struct Pipe {
   long long rs_g = 0;
   const float* dot_w = nullptr;
   int dot_n = 0;
-  double flop_div = 1.0;  // split-bf16 GEMMs do 3x the algorithmic FLOPs
+  double flop_div = 1.0;  // actual / algorithmic FLOPs of the next gemm() (profiling marks)
   GemmEpilogue ln{};      // folded-LN2 producer / consumer operands (reset after use)
   const __nv_bfloat16* resid_b = nullptr;  // bf16 residual of the next gemm()
   const float* gate_w = nullptr;           // gated-fusion vectors of the next gemm() (EPI_GATED)
@@ -683,22 +681,6 @@ struct Pipe {
     return 0;
   }
 
-  // fp32 rows -> centered bf16 rows + rstd (folded LayerNorm input)
-  int center(const float* src, long long src_gstride, Act* out, long long out_gstride, float* rs,
-             long long rs_gstride, long long rows) {
-    if (rows <= 0) return 0;
-    if constexpr (std::is_same<Act, __nv_bfloat16>::value) {
-      const int threads = 256;
-      dim3 grid(static_cast<unsigned>((rows * 32 + threads - 1) / threads), c->G);
-      mark("center_rows", 0.0, static_cast<double>(c->G) * rows * c->D * 6.0);
-      center_rows<<<grid, threads, 0, s>>>(src, c->D, src_gstride, out, c->D, out_gstride, rs, rs_gstride,
-                                           static_cast<int>(rows), c->D, c->d);
-      return check();
-    } else {
-      return fail(2, "center() is bf16-path only");
-    }
-  }
-
   int run(int mode) {
     if (int rc = assemble(mode)) return rc;
     if (mode == FLAME_INPUT_GATHER_ONLY) return 0;
@@ -710,7 +692,6 @@ struct Pipe {
     Act* QKV = act(e->QKV);
     Act* AO = act(e->AO);
     Act* Hf = act(e->Hf);
-    float* RS = e->RS;
     float* Xcur = nullptr;  // residual stream input of this layer (null at layer 0)
     static const bool fuse_gate = [] {  // FLAME_FUSE_GATE=0: separate gated-fusion pass (A/B)
       const char* v = getenv("FLAME_FUSE_GATE");
@@ -819,7 +800,7 @@ struct Pipe {
       gemm_name = "gemm_ffn_w2";
       if (kFold && last && fuse_gate) {
         // last layer: the W2 epilogue also performs the gated fusion over blocks
-        // (forward.py:143-156) and writes only the split-bf16 expert operand
+        // (forward.py:143-156) and writes only the fp32 sum, the tf32 expert operand
         resid_b = reinterpret_cast<const __nv_bfloat16*>(Y) + r0 * D;
         gate_w = c->gate_w; gate_b = c->gate_b;
         if (int rc = gemm(Hf + r0 * F, F, gF, 0, act(w.w2), F, static_cast<long long>(D) * F, static_cast<int>(nr), D, F,
@@ -1099,7 +1080,6 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
     e->Ecc = A(e->Rc * D * 2);
     e->rs_h = static_cast<float*>(A(G * e->Rh * 4));
     e->rs_c = static_cast<float*>(A(e->Rc * 4));
-    e->RS = static_cast<float*>(A(G * rows * 4));
     e->stat_parts = gemm_row_parts(D, EPI_RESID | EPI_STATS);
     e->STATS = static_cast<float*>(A(G * rows * e->stat_parts * 2 * 4));
     const size_t n_parts = gemm_row_parts(F, EPI_BIAS | EPI_GELU | EPI_ROWDOT);

@@ -112,22 +112,7 @@ __global__ void gated_fusion_rows(const float* __restrict__ xc, long long x_ld, 
       acc[3] = acc[3] + sigmoid_f(h.w * w.w + b.w) * h.w;
     }
   }
-  if constexpr (std::is_same<TOut, __nv_bfloat16>::value) {
-    // split-bf16 operand for the expert GEMM: [hi | hi | lo] (row stride 3D),
-    // paired with weights [W_hi | W_lo | W_hi] -> hi*hi + hi*lo + lo*hi
-    float hi[4], lo[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      hi[q] = __bfloat162float(__float2bfloat16_rn(acc[q]));
-      lo[q] = acc[q] - hi[q];
-    }
-    TOut* o = out + row * out_ld + c;
-    store4<TOut>(o, hi[0], hi[1], hi[2], hi[3]);
-    store4<TOut>(o + D, hi[0], hi[1], hi[2], hi[3]);
-    store4<TOut>(o + 2 * D, lo[0], lo[1], lo[2], lo[3]);
-  } else {
-    store4<TOut>(out + row * out_ld + c, acc[0], acc[1], acc[2], acc[3]);
-  }
+  store4<TOut>(out + row * out_ld + c, acc[0], acc[1], acc[2], acc[3]);
 }
 
 // Expert output, reference forward.py:165-166: sigmoid(hidden @ w2 + b2).
@@ -219,27 +204,6 @@ __device__ __forceinline__ void store_centered(__nv_bfloat16* y, const float4 (&
       store4<__nv_bfloat16>(y + c, a0, a1, a2, a3);
     }
   }
-}
-
-// fp32 rows -> centered bf16 rows + rstd (LN1 of layers > 0, LN2): one warp per row.
-__global__ void center_rows(const float* __restrict__ src, long long src_ld, long long src_gstride,
-                            __nv_bfloat16* __restrict__ out, long long out_ld, long long out_gstride,
-                            float* __restrict__ rstd, long long rs_gstride, int rows, int D, int d_true) {
-  constexpr int kChunks = 8;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  const int g = blockIdx.y;
-  if (warp >= rows) return;
-  const float* x = src + g * src_gstride + static_cast<long long>(warp) * src_ld;
-  float4 v[kChunks];
-#pragma unroll
-  for (int k = 0; k < kChunks; ++k) {
-    const int c = (k * 32 + lane) * 4;
-    v[k] = c < D ? *reinterpret_cast<const float4*>(x + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const RowStats st = warp_row_stats<kChunks>(v, lane, D, d_true);
-  store_centered<kChunks>(out + g * out_gstride + static_cast<long long>(warp) * out_ld, v, st.mean, lane, D, d_true);
-  if (lane == 0) rstd[g * rs_gstride + warp] = st.rstd;
 }
 
 // Expert head combine: score = sigmoid(sum_p partial[row][p][t] + b2[t]) over the

@@ -41,7 +41,7 @@ METRICS = {
     "l2_hit_pct": "lts__t_sector_hit_rate.pct",
 }
 
-OURS = re.compile(r"pda_|gemm_bf16|gemm_f32|sumi_attention|gated_fusion|expert_|center_rows|layer_norm_rows|scatter_emb")
+OURS = re.compile(r"pda_|gemm_bf16|gemm_f32|sumi_attention|gated_fusion|expert_|layer_norm_rows|scatter_emb")
 
 UNIT_SCALE = {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "s": 1e3,
               "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
