@@ -11,7 +11,7 @@ eng.set_table(build_item_table(5000, d), dtype="fp32")
 reqs = [(h % 5000, c % 5000) for h, c in bench.make_requests(R, H, C, 7)]
 ex = eng.executor(R, H // nb, C, with_ids=True)
 ex.stage_ids(reqs); ex.run(_lib.INPUT_IDS, graph=False); ex.stream.synchronize()
-lib = _lib.load()
+lib = _lib.load()  # needs a FLAME_DEBUG_TRACE build: FLAME_B200_LIB=dev/var_trace.so (dev/build_variant.sh trace -DFLAME_DEBUG_TRACE)
 lib.flame_debug_attn_trace.argtypes = [ctypes.c_void_p]
 buf = torch.zeros(4 * 4096, dtype=torch.int64, device="cuda")
 lib.flame_debug_attn_trace(ctypes.c_void_p(buf.data_ptr()))

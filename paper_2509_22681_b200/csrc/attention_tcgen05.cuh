@@ -57,6 +57,7 @@ __device__ unsigned long long* g_attn_trace = nullptr;
 __device__ unsigned int g_attn_trace_n[4];
 // Each slot has exactly one writer thread, which keeps its own counter
 // (trace_k, declared in each role) — no atomics on the traced path.
+#ifdef FLAME_DEBUG_TRACE
 #define ATTN_TRACE(slot, code)                                                            \
   do {                                                                                    \
     if (g_attn_trace != nullptr && blockIdx.x == 0 && ((slot) >= 2 ? (threadIdx.x & 31) == 0 : (threadIdx.x & 127) == 0)) { \
@@ -64,6 +65,9 @@ __device__ unsigned int g_attn_trace_n[4];
       ++trace_k;                                                                          \
     }                                                                                     \
   } while (0)
+#else
+#define ATTN_TRACE(slot, code) do { (void)trace_k; } while (0)
+#endif
 
 namespace attn {
 constexpr int kRows = 128;

@@ -98,6 +98,7 @@ enum : int {
 // slot 1 = epilogue warp 0, slot 2 = epilogue warp 4, slot 3 = producer;
 // entry = clock64 << 8 | code.  One writer per slot, no atomics.
 __device__ unsigned long long* g_gemm_trace = nullptr;
+#ifdef FLAME_DEBUG_TRACE
 #define GEMM_TRACE(slot, code)                                                                  \
   do {                                                                                          \
     if (g_gemm_trace != nullptr && blockIdx.x == 0 && lane == 0) {                              \
@@ -105,6 +106,9 @@ __device__ unsigned long long* g_gemm_trace = nullptr;
       ++gtrace_k;                                                                               \
     }                                                                                           \
   } while (0)
+#else
+#define GEMM_TRACE(slot, code) do { (void)gtrace_k; } while (0)
+#endif
 
 namespace gemm {
 
