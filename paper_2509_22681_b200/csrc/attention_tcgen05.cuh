@@ -266,6 +266,26 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     for (int jk = 0; cur.valid; ++jk, ++n) {
       const Job nxt = job_at(i, jk + 1);
       ATTN_TRACE(2 + i, 11);
+#ifdef FLAME_ATTN_L2_PREFETCH
+      {
+        // warm L2 two jobs ahead (the smem slots are all in use): that job's Q /
+        // K_self / V_self tiles and, for a new unit, its history K / V chunks
+        const Job far = job_at(i, jk + 2);
+        if (leader && far.valid) {
+          ptx::tma_prefetch_3d(&tm_qkv, far.h * DH, far.q_row0, far.g);
+          if (!kHist) {
+            ptx::tma_prefetch_3d(&tm_qkv, a.DA + far.h * DH, far.q_row0, far.g);
+            ptx::tma_prefetch_3d(&tm_qkv, 2 * a.DA + far.h * DH, far.q_row0, far.g);
+          }
+          if (far.u != nxt.u)
+            for (int c = 0; c < far.nk_all; ++c) {
+              ptx::tma_prefetch_3d(&tm_qkv, a.DA + far.h * DH, far.hist_row0 + c * kKeys, far.g);
+              ptx::tma_prefetch_3d(&tm_qkv, 2 * a.DA + far.h * DH, far.hist_row0 + c * kKeys, far.g);
+            }
+        }
+        __syncwarp();
+      }
+#endif
       const bool resident = cur.nk_all <= 2;
       // Q / K_self of `nxt` may load once the last S of `cur` completed and the WG
       // read its q / k_self rows (qs_free phase n)
