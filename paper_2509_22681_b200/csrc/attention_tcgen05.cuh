@@ -266,7 +266,6 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     for (int jk = 0; cur.valid; ++jk, ++n) {
       const Job nxt = job_at(i, jk + 1);
       ATTN_TRACE(2 + i, 11);
-#ifdef FLAME_ATTN_L2_PREFETCH
       {
         // warm L2 two jobs ahead (the smem slots are all in use): that job's Q /
         // K_self / V_self tiles and, for a new unit, its history K / V chunks
@@ -285,7 +284,6 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
         }
         __syncwarp();
       }
-#endif
       const bool resident = cur.nk_all <= 2;
       // Q / K_self of `nxt` may load once the last S of `cur` completed and the WG
       // read its q / k_self rows (qs_free phase n)

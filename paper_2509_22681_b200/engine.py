@@ -164,7 +164,7 @@ class DeviceExecutor:
     of the whole forward pass.  ``score`` runs H2D -> forward -> D2H."""
 
     def __init__(self, engine: FlameEngine, R: int, hb_bkt: int, c_bkt: int,
-                 with_ids: bool = False) -> None:
+                 with_ids: bool = False, pinned: bool = True) -> None:
         cfg = engine.config
         self.engine = engine
         self.R, self.hb_bkt, self.c_bkt = R, hb_bkt, c_bkt
@@ -183,7 +183,9 @@ class DeviceExecutor:
 
         def halloc(shape, dtype):
             self.allocations += 1
-            t = torch.zeros(max(1, int(np.prod(shape))), dtype=dtype, pin_memory=True)
+            # pageable staging (pinned=False) is the reference's mem_opt=off ablation:
+            # the copies then go through the driver's bounce buffer, synchronously
+            t = torch.zeros(max(1, int(np.prod(shape))), dtype=dtype, pin_memory=pinned)
             return t[: int(np.prod(shape))].view(shape)
 
         self.hist_emb = dalloc((R, self.H_bkt, d), torch.float32)
@@ -360,6 +362,10 @@ class DeviceExecutor:
 
     def ready(self) -> bool:
         return self._pending is not None and self._done.query()
+
+    def wait(self) -> None:
+        """Block until the last submitted batch (if any) finished on the device."""
+        self._done.synchronize()
 
     def collect(self) -> list[np.ndarray]:
         if self._pending is None:

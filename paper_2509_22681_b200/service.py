@@ -21,24 +21,36 @@ an empty store value does in the reference (``decode_embedding``,
 HBM at once (the incremental-refresh path of SURVEY §8f.2), so later requests
 see the new features.
 
+Concurrent callers are coalesced: while one thread's batch runs on the device,
+requests arriving from other threads queue up, and the next free caller scores
+the whole queue as one DSO batch (leader / follower, no extra thread).  The
+reference's ablation toggles map onto the device path (``ServiceConfig``,
+``config.py:53-99``): ``cache_enabled`` = features resident in the HBM item
+table (off: the host resolves every id from its store copy and ships fp32 rows),
+``mem_opt`` = pinned staging with async copies (off: pageable, synchronous),
+``routing`` = ``explicit`` DSO buckets with graphs vs ``implicit`` exact-shape
+executors built per request (reference ``ImplicitShapeRunner``).
+
 Out of scope (host harness without device arithmetic): the host
-feature cache and its staleness modes, simulated store latency, the transfer
-cost model, the HTTP layer.
+feature cache's TTL / staleness modes, simulated store latency, the transfer
+cost model.
 """
 
 from __future__ import annotations
 
 import threading
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
 from .config import ModelConfig
-from .engine import FlameEngine
+from .engine import DeviceExecutor, FlameEngine
 from .orchestrator import BucketScheduler
-from .params import ModelParams, init_params
+from .params import ModelParams, init_params, load_params
 from .pda import DEFAULT_STORE_SEED, build_item_table, item_embedding
+
+ROUTINGS = ("explicit", "implicit")
 
 
 class RequestError(ValueError):
@@ -64,11 +76,75 @@ class ScoreResponse:
     compute_latency_ms: float
 
 
+@dataclass(frozen=True)
+class ServiceConfig:
+    """The device service's deployment knobs.  ``from_dict`` reads the
+    reference's service JSON (``config.py:53-91``: ``model``, ``cache_enabled``,
+    ``mem_opt``, ``orchestrator.routing`` / ``profile_shapes``, ``params_path``);
+    keys of the reference's host harness (cache TTLs, store latency, bandwidth
+    table, listen address) are accepted and ignored."""
+
+    model: ModelConfig
+    num_items: int = 100_000
+    store_seed: int = DEFAULT_STORE_SEED
+    cache_enabled: bool = True
+    mem_opt: bool = True
+    routing: str = "explicit"
+    profile_shapes: tuple = ()  # candidate counts warmed at startup, at max_history_len
+    params_path: str | None = None
+    table_dtype: str = "fp32"
+    precision: str = "bf16"
+    target_rows: int = 16384
+    max_batch: int = 256  # requests coalesced into one dispatch
+
+    def __post_init__(self) -> None:
+        if self.routing not in ROUTINGS:
+            raise ValueError(f"routing must be one of {ROUTINGS}, got {self.routing!r}")
+        if self.num_items < 1 or self.max_batch < 1:
+            raise ValueError("num_items and max_batch must be >= 1")
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "ServiceConfig":
+        model = d["model"]
+        kw = {"model": model if isinstance(model, ModelConfig) else ModelConfig.from_dict(model)}
+        orch = d.get("orchestrator", {})
+        if "routing" in orch:
+            kw["routing"] = str(orch["routing"])
+        if "profile_shapes" in orch:
+            kw["profile_shapes"] = tuple(int(x) for x in orch["profile_shapes"])
+        for k in ("cache_enabled", "mem_opt"):
+            if k in d:
+                kw[k] = bool(d[k])
+        for k in ("num_items", "store_seed", "target_rows", "max_batch"):
+            if k in d:
+                kw[k] = int(d[k])
+        for k in ("params_path", "table_dtype", "precision", "routing"):
+            if k in d:
+                kw[k] = d[k]
+        return cls(**kw)
+
+    def with_ablation(self, cache: bool, mem_opt: bool, routing: str) -> "ServiceConfig":
+        return replace(self, cache_enabled=cache, mem_opt=mem_opt, routing=routing)
+
+
 def _percentile(values, q: float) -> float:
     """Nearest-rank percentile (reference metrics.py:11-19)."""
     s = sorted(values)
     k = max(1, int(np.ceil(q * len(s))))
     return s[k - 1]
+
+
+class _Ticket:
+    """One queued request of the coalescing dispatcher."""
+
+    __slots__ = ("hist", "cand", "scores", "lat", "error", "done")
+
+    def __init__(self, hist, cand) -> None:
+        self.hist, self.cand = hist, cand
+        self.scores = None
+        self.lat = 0.0
+        self.error = None
+        self.done = False
 
 
 class DeviceService:
@@ -77,25 +153,69 @@ class DeviceService:
     def __init__(self, config: ModelConfig, params: ModelParams | None = None, *, num_items: int = 100_000,
                  store_seed: int = DEFAULT_STORE_SEED, table: np.ndarray | None = None,
                  table_dtype: str = "fp32", precision: str = "bf16", device=None,
-                 target_rows: int = 16384) -> None:
+                 target_rows: int = 16384, cache_enabled: bool = True, mem_opt: bool = True,
+                 routing: str = "explicit", max_batch: int = 256) -> None:
+        if routing not in ROUTINGS:
+            raise ValueError(f"routing must be one of {ROUTINGS}, got {routing!r}")
         self.config = config
         self.params = params if params is not None else init_params(config)
         self.store_seed = store_seed
+        self.cache_enabled, self.mem_opt, self.routing = cache_enabled, mem_opt, routing
+        self.max_batch = max_batch
         self.engine = FlameEngine(self.params, config, precision=precision, device=device)
         if table is None:
             table = build_item_table(num_items, config.hidden_dim, store_seed)
-        self.engine.set_table(table, dtype=table_dtype)
-        self.num_items = table.shape[0]
+        # the store's current values; the device table mirrors it (cache on) or
+        # the host resolves requests from it (cache off)
+        self._store = np.array(table, dtype=np.float32)
+        self.engine.set_table(self._store, dtype=table_dtype)
+        self.num_items = self._store.shape[0]
         self._versions: dict[int, int] = {}
-        self.scheduler = BucketScheduler(self.engine, target_rows=target_rows, with_ids=True)
-        self._lock = threading.Lock()  # scoring vs. table refresh
+        self.scheduler = BucketScheduler(self.engine, target_rows=target_rows, with_ids=True, pinned=mem_opt)
+        self._lock = threading.Lock()  # device work vs. table refresh
         self._closed = False
         self._inflight = 0
         self._drained = threading.Condition(threading.Lock())
+        self._queue: list = []
+        self._leader = False
+        self._in_flight = 0  # batches taken by a leader and not yet completed
+        self._on_device = 0  # of those, batches submitted to the GPU
+        self.max_inflight = 2
+        self._cv = threading.Condition(threading.Lock())
         self._overall_ms: list = []
         self._compute_ms: list = []
+        self._stats_lock = threading.Lock()
         self.requests_total = 0
         self.pairs_processed = 0
+        self.lookups = 0
+        self.hits = 0
+        self.feature_bytes = 0  # feature data moved host -> device (ids, rows, refreshes)
+        self.dispatches = 0  # coalesced batches run
+        self._implicit_allocs = 0
+        self._alloc_base = 0
+
+    @classmethod
+    def from_config(cls, cfg: ServiceConfig, device=None) -> "DeviceService":
+        params = None
+        if cfg.params_path:
+            file_cfg, params = load_params(cfg.params_path)
+            if file_cfg != cfg.model:
+                raise ValueError(f"{cfg.params_path} holds parameters of a different model config")
+        svc = cls(cfg.model, params, num_items=cfg.num_items, store_seed=cfg.store_seed,
+                  table_dtype=cfg.table_dtype, precision=cfg.precision, device=device,
+                  target_rows=cfg.target_rows, cache_enabled=cfg.cache_enabled, mem_opt=cfg.mem_opt,
+                  routing=cfg.routing, max_batch=cfg.max_batch)
+        if cfg.profile_shapes:
+            svc.warm([(cfg.model.max_history_len, c) for c in cfg.profile_shapes])
+        return svc
+
+    def warm(self, shapes) -> None:
+        """Build the executors of the buckets of ``shapes`` ((H, C) pairs) now;
+        allocations after the last ``warm`` count as steady-state allocations."""
+        if self.routing == "explicit":
+            with self._lock:
+                self.scheduler.warm(shapes)
+                self._alloc_base = self.scheduler.allocations
 
     # -- request path ---------------------------------------------------------
 
@@ -117,8 +237,8 @@ class DeviceService:
         return self.handle_batch([req])[0]
 
     def handle_batch(self, reqs) -> list[ScoreResponse]:
-        """Score many requests at once through the DSO; per-request latencies are
-        from the call to the collection of the request's group."""
+        """Score many requests at once; per-request compute latency runs from the
+        dispatch of the request's batch to the collection of its group."""
         t0 = time.perf_counter()
         for r in reqs:
             self._validate(r)
@@ -127,25 +247,150 @@ class DeviceService:
                 raise ServiceClosedError("service is shut down")
             self._inflight += 1
         try:
-            batch = [(np.asarray(r.history_item_ids, dtype=np.int64), np.asarray(r.candidate_item_ids, dtype=np.int64))
-                     for r in reqs]
-            with self._lock:
-                t1 = time.perf_counter()
-                scores = self.scheduler.score(batch, ids=True)
-                lat = list(self.scheduler.last_latencies)
-            out = []
-            for r, s, l in zip(reqs, scores, lat):
-                overall = (t1 - t0 + l) * 1000.0
-                out.append(ScoreResponse(s, overall, l * 1000.0))
-                self._overall_ms.append(overall)
-                self._compute_ms.append(l * 1000.0)
-                self.requests_total += 1
-                self.pairs_processed += len(r.candidate_item_ids)
+            tickets = [_Ticket(np.asarray(r.history_item_ids, dtype=np.int64),
+                               np.asarray(r.candidate_item_ids, dtype=np.int64)) for r in reqs]
+            self._dispatch(tickets)
+            for t in tickets:
+                if t.error is not None:
+                    raise t.error
+            t1 = time.perf_counter()
+            out = [ScoreResponse(t.scores, (t1 - t0) * 1000.0, t.lat * 1000.0) for t in tickets]
+            with self._stats_lock:
+                for r, o in zip(reqs, out):
+                    self._overall_ms.append(o.overall_latency_ms)
+                    self._compute_ms.append(o.compute_latency_ms)
+                    self.requests_total += 1
+                    self.pairs_processed += len(r.candidate_item_ids)
             return out
         finally:
             with self._drained:
                 self._inflight -= 1
                 self._drained.notify_all()
+
+    def _dispatch(self, tickets) -> None:
+        """Leader / follower coalescing with up to ``max_inflight`` batches on the
+        device: the tickets are queued; a caller that finds no submission in
+        progress and a free in-flight slot takes up to ``max_batch`` queued
+        tickets (anyone's), submits them, hands the leader role on, then waits
+        for that batch and completes its tickets.  While one batch runs on the
+        GPU the next one is staged and submitted, and requests that arrive
+        meanwhile form the batch after it."""
+        with self._cv:
+            self._queue.extend(tickets)
+        while True:
+            with self._cv:
+                self._cv.wait_for(lambda: all(t.done for t in tickets)
+                                  or (self._queue and not self._leader and self._in_flight < self.max_inflight))
+                if all(t.done for t in tickets):
+                    return
+                self._leader = True
+            owned = []
+            try:
+                while True:  # submit while there is queued work and an in-flight slot
+                    with self._cv:
+                        if not self._queue or self._in_flight >= self.max_inflight:
+                            break
+                        self._in_flight += 1
+                        batch, self._queue = self._queue[: self.max_batch], self._queue[self.max_batch:]
+                    try:
+                        owned.append((batch, self._submit(batch)))
+                    except BaseException as exc:  # noqa: BLE001 - surfaced to each ticket's caller
+                        for t in batch:
+                            t.error = exc
+                        owned.append((batch, None))
+            finally:
+                with self._cv:
+                    self._leader = False
+                    self._cv.notify_all()
+            for batch, handle in owned:
+                try:
+                    if handle is not None:
+                        self._complete(batch, handle)
+                except BaseException as exc:  # noqa: BLE001
+                    for t in batch:
+                        t.error = exc
+                finally:
+                    with self._cv:
+                        for t in batch:
+                            t.done = True
+                        self._in_flight -= 1
+                        self._cv.notify_all()
+
+    def _host_rows(self, ids: np.ndarray) -> np.ndarray:
+        """The store's rows for ``ids`` (zeros for unknown ids), resolved on the host."""
+        rows = np.zeros((ids.size, self.config.hidden_dim), dtype=np.float32)
+        ok = (ids >= 0) & (ids < self.num_items)
+        rows[ok] = self._store[ids[ok]]
+        return rows
+
+    def _submit(self, batch):
+        """Resolve the batch's features and submit it (explicit routing), or run
+        it to completion (implicit routing).  Returns what ``_complete`` needs."""
+        d = self.config.hidden_dim
+        n_ids = sum(t.hist.size + t.cand.size for t in batch)
+        if self.cache_enabled:
+            hits = sum(int(np.count_nonzero((t.hist >= 0) & (t.hist < self.num_items)))
+                       + int(np.count_nonzero((t.cand >= 0) & (t.cand < self.num_items))) for t in batch)
+            work = [(t.hist, t.cand) for t in batch]
+            nbytes = 8 * n_ids
+        else:
+            hits = 0
+            work = [(self._host_rows(t.hist), self._host_rows(t.cand)) for t in batch]
+            nbytes = 4 * d * n_ids
+        with self._stats_lock:
+            self.dispatches += 1
+            self.lookups += n_ids
+            self.hits += hits
+            self.feature_bytes += nbytes
+        with self._lock:
+            if self.routing == "explicit":
+                rec = self.scheduler.submit_batch(work, ids=self.cache_enabled)
+                with self._cv:
+                    self._on_device += 1
+                return ("rec", rec)
+            return ("done", [self._run_implicit(h, c) for h, c in work])
+
+    def _complete(self, batch, handle) -> None:
+        kind, obj = handle
+        if kind == "rec":
+            try:
+                scores, lat = self.scheduler.collect_batch(obj)
+            finally:
+                with self._cv:
+                    self._on_device -= 1
+                    self._cv.notify_all()
+        else:
+            scores, lat = [s for s, _ in obj], [l for _, l in obj]
+        for t, s, l in zip(batch, scores, lat):
+            t.scores, t.lat = s, l
+
+    def _quiesce(self) -> None:
+        """Wait until no batch is on the device (caller holds ``_lock``, so no
+        new batch can be submitted)."""
+        with self._cv:
+            self._cv.wait_for(lambda: self._on_device == 0)
+
+    def _run_implicit(self, hist, cand):
+        """Reference ImplicitShapeRunner (orchestrator.py:225-260): exact-shape
+        buffers allocated for the request, eager launch, released afterwards."""
+        ex = DeviceExecutor(self.engine, 1, len(hist) // self.config.num_blocks, len(cand),
+                            with_ids=self.cache_enabled, pinned=self.mem_opt)
+        self._implicit_allocs += ex.allocations
+        try:
+            t0 = time.perf_counter()
+            if self.cache_enabled:
+                s = ex.score_ids([(hist, cand)], graph=False)[0]
+            else:
+                s = ex.score([(hist, cand)], graph=False)[0]
+            return s, time.perf_counter() - t0
+        finally:
+            ex.close()
+
+    @property
+    def steady_state_allocations(self) -> int:
+        if self.routing == "implicit":
+            return self._implicit_allocs
+        return self.scheduler.allocations - self._alloc_base
 
     # -- feature path ---------------------------------------------------------
 
@@ -166,27 +411,46 @@ class DeviceService:
             self._versions[i] = self._versions.get(i, 0) + 1
         rows = np.stack([self.embedding_of(i) for i in ids])
         with self._lock:
+            self._quiesce()
+            self._store[ids] = rows
             self.engine.update_rows(np.asarray(ids, dtype=np.int64), rows)
+        with self._stats_lock:
+            self.feature_bytes += rows.size * 4
 
     def refresh_values(self, item_ids, values) -> None:
         """Write raw store feature values (reference wire format, store.py:66-78:
         float64 LE embedding + filler; empty -> zero row) into the device table,
         decoded on the GPU — the path a store feed / cache refresh would use."""
+        ids = np.asarray(item_ids, dtype=np.int64).reshape(-1)
+        values = list(values)
+        d = self.config.hidden_dim
         with self._lock:
-            self.engine.update_values(np.asarray(item_ids, dtype=np.int64), list(values))
+            self._quiesce()
+            self.engine.update_values(ids, values)
+            for i, v in zip(ids, values):
+                if 0 <= i < self.num_items:
+                    self._store[i] = np.frombuffer(v[: 8 * d], dtype="<f8") if len(v) >= 8 * d else 0.0
+        with self._stats_lock:
+            self.feature_bytes += sum(len(v) for v in values)
 
     # -- observability / lifecycle --------------------------------------------
 
     def metrics_snapshot(self) -> dict:
+        """Reference /metrics fields (api.py:60-66): request counts, latency
+        summaries, cache hit rate, feature bytes moved, steady-state allocations."""
         def summary(series):
             if not series:
                 return {"count": 0}
             return {"count": len(series), "mean": sum(series) / len(series),
                     "p50": _percentile(series, 0.5), "p99": _percentile(series, 0.99)}
 
-        return {"requests_total": self.requests_total, "pairs_processed": self.pairs_processed,
-                "overall_ms": summary(self._overall_ms), "compute_ms": summary(self._compute_ms),
-                "steady_state_allocs": 0}
+        with self._stats_lock:
+            return {"requests_total": self.requests_total, "pairs_processed": self.pairs_processed,
+                    "overall_ms": summary(self._overall_ms), "compute_ms": summary(self._compute_ms),
+                    "cache": {"enabled": self.cache_enabled, "lookups": self.lookups,
+                              "hit_rate": self.hits / self.lookups if self.lookups else 0.0},
+                    "network_bytes": self.feature_bytes, "dispatches": self.dispatches,
+                    "steady_state_allocs": self.steady_state_allocations}
 
     def close(self, drain_timeout_s: float = 30.0) -> None:
         """Stop accepting requests and wait for in-flight ones (service.py:222-233)."""
