@@ -21,6 +21,7 @@ k = list(csv.DictReader(open(P / "ncu_kernels_cfg3.csv")))
 krows = [f"| {x['role']} | {float(x['duration_ms']):.3f} | {100 * float(x['share']):.0f} % | "
          f"{float(x['dram_read_MB']):.0f} / {float(x['dram_write_MB']):.0f} | {float(x['dram_pct']):.0f} | "
          f"{float(x['tensor_pct']):.0f} | {float(x['issue_pct']):.0f} |" for x in k]
+att_mb = next(float(x["dram_read_MB"]) for x in k if x["role"] == "attention_sumi")
 par = json.loads((P / "parity.json").read_text())
 ref = json.loads((P / "reference_arm_cfg3.json").read_text())
 d3 = json.loads((P / "bench_cfg3.json").read_text())
@@ -63,11 +64,13 @@ reasons {d3['clocks']['reasons']}.
 
 How to read the table:
 * The gated fusion over the Climber blocks runs inside the FFN W2 epilogue. W2 writes
-  93 MB, the split-bf16 expert operand, instead of 537 MB of fp32 block outputs.
-* The attention kernel reads exactly the algorithmic 1.07 GB: the candidates' Q,
-  K_self and V_self, plus each request-block's history K/V. The history K/V is read
-  once per (request, block, head), never per candidate. Against the HBM roofline it
-  runs at about 62 % of the measured copy bandwidth.
+  64 MB, the fp32 fused rows (the tf32 expert operand), instead of 537 MB of fp32
+  block outputs.
+* The attention kernel's algorithmic read is 1.07 GB: the candidates' Q, K_self and
+  V_self, plus each request-block's history K/V. The history K/V is read once per
+  (request, block, head), never per candidate. In this cold, serialised capture it
+  reads {att_mb / 1000:.2f} GB; the excess is tiles its L2 prefetch of the
+  next-but-one job fetched and lost before use.
 * The K = 512 projection GEMMs run as CTA pairs, which halves each CTA's W-tile L2
   traffic.
 * PDA: the radix-sort dedup and the run-piece gather together take about 0.1 ms.
