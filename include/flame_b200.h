@@ -101,6 +101,15 @@ int flame_update_table(FlameCtx* ctx, const long long* host_ids, const float* ho
 int flame_update_table_values(FlameCtx* ctx, const long long* host_ids, const void* host_values,
                               long long value_stride, const int* host_value_len, long long n, void* stream);
 
+/* Host staging helper: n variable-length records stored back to back in `flat`
+ * (record i = lens[i] elements of elem_bytes bytes) are copied into fixed-stride
+ * slots, record i at dst + i * dst_stride_bytes.  Fills an executor's pinned id /
+ * row mirrors with one call per batch instead of one copy per request (the
+ * reference copies each request into its executor's preallocated buffers,
+ * orchestrator.py:209-213).  Returns 1 if a record exceeds its slot. */
+int flame_pack_padded(void* dst, long long dst_stride_bytes, const void* flat, const long long* lens, long long n,
+                      long long elem_bytes);
+
 /* Capacity of one id list in the unique/inverse buffers: max(H_bkt, C_bkt). */
 int flame_exec_list_capacity(int num_blocks, int hb_bkt, int c_bkt);
 int flame_exec_create(FlameCtx* ctx, int R, int hb_bkt, int c_bkt, const FlameIO* io,

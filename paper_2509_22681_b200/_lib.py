@@ -21,7 +21,7 @@ TABLE_BF16, TABLE_FP32 = 0, 1
 
 EXPORTED = (
     "flame_create", "flame_create_flmp", "flame_destroy", "flame_set_table", "flame_update_table",
-    "flame_update_table_values",
+    "flame_update_table_values", "flame_pack_padded",
     "flame_exec_list_capacity", "flame_exec_create", "flame_exec_destroy", "flame_exec_run",
     "flame_exec_capture", "flame_exec_replay", "flame_exec_launch_count", "flame_exec_workspace",
     "flame_exec_profile",
@@ -65,6 +65,7 @@ def load() -> ctypes.CDLL:
             "flame_set_table": (I, [P, P, LL, I]),
             "flame_update_table": (I, [P, P, P, LL, P]),
             "flame_update_table_values": (I, [P, P, P, LL, P, LL, P]),
+            "flame_pack_padded": (I, [P, LL, P, P, LL, LL]),
             "flame_exec_list_capacity": (I, [I, I, I]),
             "flame_exec_create": (I, [P, I, I, I, ctypes.POINTER(FlameIO), ctypes.POINTER(P)]),
             "flame_exec_destroy": (I, [P]),

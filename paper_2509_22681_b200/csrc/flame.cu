@@ -1043,6 +1043,23 @@ int flame_update_table_values(FlameCtx* c, const long long* host_ids, const void
   return 0;
 }
 
+int flame_pack_padded(void* dst, long long dst_stride_bytes, const void* flat, const long long* lens, long long n,
+                      long long elem_bytes) {
+  if (n < 0 || elem_bytes <= 0 || dst_stride_bytes < 0 || (n > 0 && (!dst || !lens))) return fail(1, "bad pack arguments");
+  const uint8_t* src = static_cast<const uint8_t*>(flat);
+  uint8_t* out = static_cast<uint8_t*>(dst);
+  for (long long i = 0; i < n; ++i) {
+    const long long bytes = lens[i] * elem_bytes;
+    if (lens[i] < 0 || bytes > dst_stride_bytes) return fail(1, "record longer than its slot");
+    if (bytes) {
+      if (!src) return fail(1, "bad pack arguments");
+      std::memcpy(out + i * dst_stride_bytes, src, static_cast<size_t>(bytes));
+      src += bytes;
+    }
+  }
+  return 0;
+}
+
 int flame_exec_list_capacity(int num_blocks, int hb_bkt, int c_bkt) {
   const int H = num_blocks * hb_bkt;
   return H > c_bkt ? H : c_bkt;

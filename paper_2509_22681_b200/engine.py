@@ -252,6 +252,7 @@ class DeviceExecutor:
         meta[2, :n] = offs[:n]
         meta[3, 0] = n  # slots n..R-1 are skipped by the kernels (one graph serves any n <= R)
         self.n_real = int(np.sum(cand_lens))
+        self._counts = np.asarray(cand_lens, dtype=np.int64)
         return n
 
     def _check_lengths(self, h: int, c: int) -> None:
@@ -263,17 +264,41 @@ class DeviceExecutor:
         if not 1 <= c <= self.c_bkt:
             raise ValueError(f"candidate count {c} outside [1, {self.c_bkt}]")
 
+    def _lengths(self, requests) -> tuple[np.ndarray, np.ndarray]:
+        """Per-request (H, C) as int64 arrays, validated against the executor."""
+        n = len(requests)
+        if n > self.R:
+            raise ValueError(f"{n} requests exceed executor capacity {self.R}")
+        hl = np.fromiter((len(h) for h, _ in requests), dtype=np.int64, count=n)
+        cl = np.fromiter((len(c) for _, c in requests), dtype=np.int64, count=n)
+        bad = np.flatnonzero((hl % self.engine.config.num_blocks != 0) | (hl > self.H_bkt) | (cl < 1)
+                             | (cl > self.c_bkt))
+        if bad.size:
+            self._check_lengths(int(hl[bad[0]]), int(cl[bad[0]]))  # raises the specific error
+        return hl, cl
+
+    def _pack(self, dst: torch.Tensor, arrays, lens: np.ndarray, dtype, width: int = 0) -> None:
+        """Copy the requests' arrays into the pinned mirror ``dst`` ([R][slot...]),
+        one C call for the batch (flame_pack_padded)."""
+        if not lens.any():
+            return
+        parts = [a for a, l in zip(arrays, lens) if l]
+        flat = np.concatenate(parts, dtype=dtype, casting="unsafe") if len(parts) > 1 \
+            else np.asarray(parts[0], dtype=dtype)
+        if width and (flat.ndim != 2 or flat.shape[1] != width):
+            raise ValueError(f"embedding rows must have hidden_dim {width} columns, got shape {flat.shape[1:]}")
+        flat = np.ascontiguousarray(flat)
+        lens = np.ascontiguousarray(lens, dtype=np.int64)
+        elem = flat.itemsize * (width or 1)
+        _lib.check(self.engine.lib.flame_pack_padded(dst.data_ptr(), dst.stride(0) * dst.element_size(),
+                                                     flat.ctypes.data, lens.ctypes.data, lens.size, elem))
+
     def stage_embeddings(self, requests) -> None:
         """requests: sequence of (history (H, d), candidates (C, d)) arrays."""
-        hl, cl = [], []
-        hh, hc = self.h_hist.numpy(), self.h_cand.numpy()
-        for r, (hist, cand) in enumerate(requests):
-            h, c = hist.shape[0], cand.shape[0]
-            self._check_lengths(h, c)
-            hh[r, :h] = hist
-            hc[r, :c] = cand
-            hl.append(h)
-            cl.append(c)
+        hl, cl = self._lengths(requests)
+        d = self.engine.config.hidden_dim
+        self._pack(self.h_hist, [h for h, _ in requests], hl, np.float32, d)
+        self._pack(self.h_cand, [c for _, c in requests], cl, np.float32, d)
         n = self._set_meta(hl, cl)
         with torch.cuda.stream(self.stream):
             self.hist_emb[:n].copy_(self.h_hist[:n], non_blocking=True)
@@ -284,17 +309,9 @@ class DeviceExecutor:
         """requests: sequence of (history ids (H,), candidate ids (C,)) int arrays."""
         if not self.with_ids:
             raise RuntimeError("executor was built without id buffers")
-        if len(requests) > self.R:
-            raise ValueError(f"{len(requests)} requests exceed executor capacity {self.R}")
-        hl, cl = [], []
-        hh, hc = self.h_hist_ids.numpy(), self.h_cand_ids.numpy()
-        for r, (hist, cand) in enumerate(requests):
-            h, c = len(hist), len(cand)
-            self._check_lengths(h, c)
-            hh[r, :h] = hist
-            hc[r, :c] = cand
-            hl.append(h)
-            cl.append(c)
+        hl, cl = self._lengths(requests)
+        self._pack(self.h_hist_ids, [h for h, _ in requests], hl, np.int64)
+        self._pack(self.h_cand_ids, [c for _, c in requests], cl, np.int64)
         n = self._set_meta(hl, cl)
         with torch.cuda.stream(self.stream):
             # only the slots in use cross PCIe (the kernels skip the others)
@@ -354,7 +371,7 @@ class DeviceExecutor:
         with torch.cuda.stream(self.stream):
             self.h_scores[:n].copy_(self.scores[:n], non_blocking=True)
             self._done.record(self.stream)
-        self._pending = [len(c) for _, c in requests]
+        self._pending = self._counts
 
     @property
     def pending(self) -> bool:

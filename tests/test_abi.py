@@ -75,3 +75,25 @@ def test_sm100a_code_in_library():
                           text=True, check=True).stdout
     assert "sm_100a" in sass
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+
+
+def test_pack_padded_host_staging():
+    """flame_pack_padded (host-only): ragged records into fixed-stride slots,
+    empty records skipped, an oversize record rejected (status 1)."""
+    lib = _lib.load()
+    recs = [np.arange(5, dtype=np.int64), np.zeros(0, dtype=np.int64), np.arange(100, 108, dtype=np.int64)]
+    lens = np.array([len(r) for r in recs], dtype=np.int64)
+    flat = np.concatenate(recs)
+    dst = np.full((3, 8), -1, dtype=np.int64)
+    assert lib.flame_pack_padded(dst.ctypes.data, 64, flat.ctypes.data, lens.ctypes.data, 3, 8) == 0
+    np.testing.assert_array_equal(dst[0, :5], recs[0])
+    assert (dst[0, 5:] == -1).all() and (dst[1] == -1).all()
+    np.testing.assert_array_equal(dst[2], recs[2])
+    rows = np.random.default_rng(0).standard_normal((6, 4)).astype(np.float32)
+    out = np.zeros((2, 5, 4), dtype=np.float32)
+    rl = np.array([2, 4], dtype=np.int64)
+    assert lib.flame_pack_padded(out.ctypes.data, 80, rows.ctypes.data, rl.ctypes.data, 2, 16) == 0
+    np.testing.assert_array_equal(out[0, :2], rows[:2])
+    np.testing.assert_array_equal(out[1, :4], rows[2:])
+    big = np.array([9], dtype=np.int64)
+    assert lib.flame_pack_padded(dst.ctypes.data, 64, np.zeros(9, np.int64).ctypes.data, big.ctypes.data, 1, 8) == 1

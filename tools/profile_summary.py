@@ -60,7 +60,7 @@ reasons {d3['clocks']['reasons']}.
 
 | kernel | ms | share | DRAM R/W MB | DRAM % | tensor % | issue % |
 |---|---|---|---|---|---|---|
-""" + "\n".join(krows) + """
+""" + "\n".join(krows) + f"""
 
 How to read the table:
 * The gated fusion over the Climber blocks runs inside the FFN W2 epilogue. W2 writes
