@@ -233,12 +233,6 @@ class DeviceExecutor:
             _lib.check(engine.lib.flame_exec_create(engine.handle, R, hb_bkt, c_bkt, ctypes.byref(io),
                                                     ctypes.byref(ex)))
         self._ex = ex
-        st = _lib.FlameStaging(self.h_meta.data_ptr(), self.meta.data_ptr(),
-                               ptr(self.h_hist_ids) if with_ids else None,
-                               ptr(self.h_cand_ids) if with_ids else None,
-                               self.h_hist.data_ptr(), self.h_cand.data_ptr(), self.h_scores.data_ptr())
-        _lib.check(engine.lib.flame_exec_set_staging(ex, ctypes.byref(st)))
-        self._native = False
         self._graph_mode = None
         self._finalizer = weakref.finalize(self, engine.lib.flame_exec_destroy, ex)
         self.n_real = 0
@@ -299,24 +293,13 @@ class DeviceExecutor:
         _lib.check(self.engine.lib.flame_pack_padded(dst.data_ptr(), dst.stride(0) * dst.element_size(),
                                                      flat.ctypes.data, lens.ctypes.data, lens.size, elem))
 
-    def _fill_embeddings(self, requests) -> int:
+    def stage_embeddings(self, requests) -> None:
+        """requests: sequence of (history (H, d), candidates (C, d)) arrays."""
         hl, cl = self._lengths(requests)
         d = self.engine.config.hidden_dim
         self._pack(self.h_hist, [h for h, _ in requests], hl, np.float32, d)
         self._pack(self.h_cand, [c for _, c in requests], cl, np.float32, d)
-        return self._set_meta(hl, cl)
-
-    def _fill_ids(self, requests) -> int:
-        if not self.with_ids:
-            raise RuntimeError("executor was built without id buffers")
-        hl, cl = self._lengths(requests)
-        self._pack(self.h_hist_ids, [h for h, _ in requests], hl, np.int64)
-        self._pack(self.h_cand_ids, [c for _, c in requests], cl, np.int64)
-        return self._set_meta(hl, cl)
-
-    def stage_embeddings(self, requests) -> None:
-        """requests: sequence of (history (H, d), candidates (C, d)) arrays."""
-        n = self._fill_embeddings(requests)
+        n = self._set_meta(hl, cl)
         with torch.cuda.stream(self.stream):
             self.hist_emb[:n].copy_(self.h_hist[:n], non_blocking=True)
             self.cand_emb[:n].copy_(self.h_cand[:n], non_blocking=True)
@@ -324,7 +307,12 @@ class DeviceExecutor:
 
     def stage_ids(self, requests) -> None:
         """requests: sequence of (history ids (H,), candidate ids (C,)) int arrays."""
-        n = self._fill_ids(requests)
+        if not self.with_ids:
+            raise RuntimeError("executor was built without id buffers")
+        hl, cl = self._lengths(requests)
+        self._pack(self.h_hist_ids, [h for h, _ in requests], hl, np.int64)
+        self._pack(self.h_cand_ids, [c for _, c in requests], cl, np.int64)
+        n = self._set_meta(hl, cl)
         with torch.cuda.stream(self.stream):
             # only the slots in use cross PCIe (the kernels skip the others)
             self.hist_ids[:n].copy_(self.h_hist_ids[:n], non_blocking=True)
@@ -370,30 +358,19 @@ class DeviceExecutor:
     def submit(self, requests, ids: bool, graph: bool = True) -> None:
         """Stage a batch, replay the forward pass and queue the score D2H, all on
         this executor's stream, without waiting.  ``collect`` returns the scores.
-        With ``graph`` the round trip is one C call (flame_exec_submit: H2D of the
-        slots in use, graph replay, D2H, completion event).  The pinned staging
-        buffers are reused, so a second ``submit`` must come after the first
-        ``collect`` (the DSO keeps a ring of executors per bucket)."""
+        The pinned staging buffers are reused, so a second ``submit`` must come
+        after the first ``collect`` (the DSO keeps a ring of executors per bucket)."""
         if self._pending is not None:
             raise RuntimeError("executor has an uncollected batch")
-        mode = _lib.INPUT_IDS if ids else _lib.INPUT_EMBEDDINGS
-        if graph:
-            n = self._fill_ids(requests) if ids else self._fill_embeddings(requests)
-            _lib.check(self.engine.lib.flame_exec_submit(self._ex, mode, n, self.n_real,
-                                                         ctypes.c_void_p(self.stream.cuda_stream)))
-            self._graph_mode = mode
-            self._native = True
+        if ids:
+            self.stage_ids(requests)
         else:
-            if ids:
-                self.stage_ids(requests)
-            else:
-                self.stage_embeddings(requests)
-            self.run(mode, graph=False)
-            n = self.n_real
-            with torch.cuda.stream(self.stream):
-                self.h_scores[:n].copy_(self.scores[:n], non_blocking=True)
-                self._done.record(self.stream)
-            self._native = False
+            self.stage_embeddings(requests)
+        self.run(_lib.INPUT_IDS if ids else _lib.INPUT_EMBEDDINGS, graph)
+        n = self.n_real
+        with torch.cuda.stream(self.stream):
+            self.h_scores[:n].copy_(self.scores[:n], non_blocking=True)
+            self._done.record(self.stream)
         self._pending = self._counts
 
     @property
@@ -401,28 +378,16 @@ class DeviceExecutor:
         return self._pending is not None
 
     def ready(self) -> bool:
-        if self._pending is None:
-            return False
-        if not self._native:
-            return self._done.query()
-        rc = self.engine.lib.flame_exec_query(self._ex)
-        if rc not in (0, 1):
-            _lib.check(rc)
-        return rc == 1
+        return self._pending is not None and self._done.query()
 
     def wait(self) -> None:
         """Block until the last submitted batch (if any) finished on the device."""
-        if self._pending is None:
-            return
-        if self._native:
-            _lib.check(self.engine.lib.flame_exec_wait(self._ex))
-        else:
-            self._done.synchronize()
+        self._done.synchronize()
 
     def collect(self) -> list[np.ndarray]:
         if self._pending is None:
             raise RuntimeError("nothing submitted")
-        self.wait()
+        self._done.synchronize()
         counts, self._pending = self._pending, None
         flat = self.h_scores[: self.n_real].numpy().astype(np.float64)
         return _split_rows(flat, counts)

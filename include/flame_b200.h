@@ -116,6 +116,30 @@ int flame_exec_create(FlameCtx* ctx, int R, int hb_bkt, int c_bkt, const FlameIO
                       FlameExec** out);
 int flame_exec_destroy(FlameExec* ex);
 int flame_exec_run(FlameExec* ex, int input_mode, void* stream);
+/* Pinned host mirrors of an executor's inputs and scores, registered once, so
+ * that one flame_exec_submit per batch does the whole round trip (the
+ * reference's Executor.bound_run, orchestrator.py:127-131, from the caller's
+ * arrays to its scores).  Unused pointers (e.g. ids in embedding-only use) may
+ * be NULL.  h_meta / d_meta: the [4][R] int32 block whose rows are the FlameIO
+ * hist_len, cand_len, out_offset pointers and whose [3][0] is `active`. */
+typedef struct FlameStaging {
+  const void* h_meta;
+  void* d_meta;
+  const long long* h_hist_ids;  /* [R][H_bkt] */
+  const long long* h_cand_ids;  /* [R][C_bkt] */
+  const float* h_hist_emb;      /* [R][H_bkt][hidden_dim] */
+  const float* h_cand_emb;      /* [R][C_bkt][hidden_dim] */
+  float* h_scores;              /* [R*C_bkt][num_tasks] */
+} FlameStaging;
+int flame_exec_set_staging(FlameExec* ex, const FlameStaging* staging);
+/* Stream-ordered on `stream`: copy the first n_req slots of the inputs of
+ * input_mode and the metadata block to the device, run the pass (the CUDA graph,
+ * captured on first use per input mode), copy n_score_rows score rows back, and
+ * record the executor's completion event.  Returns without waiting. */
+int flame_exec_submit(FlameExec* ex, int input_mode, int n_req, long long n_score_rows, void* stream);
+/* Wait for (1) / poll (returns 1 done, 0 pending) the last flame_exec_submit. */
+int flame_exec_wait(FlameExec* ex);
+int flame_exec_query(FlameExec* ex);
 int flame_exec_capture(FlameExec* ex, int input_mode, void* stream);
 int flame_exec_replay(FlameExec* ex, void* stream);
 /* Eager run with a CUDA event recorded on `stream` before every launch.

@@ -21,7 +21,8 @@ TABLE_BF16, TABLE_FP32 = 0, 1
 
 EXPORTED = (
     "flame_create", "flame_create_flmp", "flame_destroy", "flame_set_table", "flame_update_table",
-    "flame_update_table_values", "flame_pack_padded",
+    "flame_update_table_values", "flame_pack_padded", "flame_exec_set_staging", "flame_exec_submit",
+    "flame_exec_wait", "flame_exec_query",
     "flame_exec_list_capacity", "flame_exec_create", "flame_exec_destroy", "flame_exec_run",
     "flame_exec_capture", "flame_exec_replay", "flame_exec_launch_count", "flame_exec_workspace",
     "flame_exec_profile",
@@ -39,6 +40,11 @@ class FlameIO(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "hist_emb", "cand_emb", "hist_ids", "cand_ids", "hist_len", "cand_len", "out_offset",
         "scores", "unique_ids", "inverse", "n_unique", "active")]
+
+
+class FlameStaging(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "h_meta", "d_meta", "h_hist_ids", "h_cand_ids", "h_hist_emb", "h_cand_emb", "h_scores")]
 
 
 _lib = None
@@ -66,6 +72,10 @@ def load() -> ctypes.CDLL:
             "flame_update_table": (I, [P, P, P, LL, P]),
             "flame_update_table_values": (I, [P, P, P, LL, P, LL, P]),
             "flame_pack_padded": (I, [P, LL, P, P, LL, LL]),
+            "flame_exec_set_staging": (I, [P, ctypes.POINTER(FlameStaging)]),
+            "flame_exec_submit": (I, [P, I, I, LL, P]),
+            "flame_exec_wait": (I, [P]),
+            "flame_exec_query": (I, [P]),
             "flame_exec_list_capacity": (I, [I, I, I]),
             "flame_exec_create": (I, [P, I, I, I, ctypes.POINTER(FlameIO), ctypes.POINTER(P)]),
             "flame_exec_destroy": (I, [P]),

@@ -172,8 +172,12 @@ struct FlameExec {
   int graph_mode = -1;
   int launches = 0;
   std::vector<void*> allocs;
+  FlameStaging stg{};
+  bool has_stg = false;
+  cudaEvent_t done_ev = nullptr;
 
   ~FlameExec() {
+    if (done_ev) cudaEventDestroy(done_ev);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
     for (void* p : allocs) cudaFree(p);
@@ -1187,6 +1191,65 @@ int flame_exec_replay(FlameExec* e, void* stream) {
   if (!e || !e->graph_exec) return fail(1, "executor has no captured graph");
   CUDA_TRY(cudaGraphLaunch(e->graph_exec, static_cast<cudaStream_t>(stream)));
   return 0;
+}
+
+int flame_exec_set_staging(FlameExec* e, const FlameStaging* st) {
+  if (!e || !st || !st->h_meta || !st->d_meta || !st->h_scores) return fail(1, "bad staging arguments");
+  CUDA_TRY(cudaSetDevice(e->ctx->device));
+  if (!e->done_ev) CUDA_TRY(cudaEventCreateWithFlags(&e->done_ev, cudaEventDisableTiming));
+  e->stg = *st;
+  e->has_stg = true;
+  return 0;
+}
+
+int flame_exec_submit(FlameExec* e, int mode, int n_req, long long n_score_rows, void* stream) {
+  if (!e || !e->has_stg) return fail(1, "executor has no staging buffers (flame_exec_set_staging)");
+  if (n_req < 0 || n_req > e->R || n_score_rows < 0 || n_score_rows > static_cast<long long>(e->R) * e->c_bkt)
+    return fail(1, "batch exceeds executor capacity");
+  const FlameStaging& st = e->stg;
+  const bool ids = mode == FLAME_INPUT_IDS;
+  if (ids ? (!st.h_hist_ids || !st.h_cand_ids || !e->io.hist_ids || !e->io.cand_ids)
+          : (!st.h_hist_emb || !st.h_cand_emb || !e->io.hist_emb || !e->io.cand_emb))
+    return fail(1, "no staging buffers for this input mode");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long n = n_req;
+  const long long hrow = ids ? e->H_bkt * 8LL : e->H_bkt * 4LL * e->ctx->d;
+  const long long crow = ids ? e->c_bkt * 8LL : e->c_bkt * 4LL * e->ctx->d;
+  void* dh = ids ? static_cast<void*>(const_cast<long long*>(e->io.hist_ids))
+                 : static_cast<void*>(const_cast<float*>(e->io.hist_emb));
+  void* dc = ids ? static_cast<void*>(const_cast<long long*>(e->io.cand_ids))
+                 : static_cast<void*>(const_cast<float*>(e->io.cand_emb));
+  const void* hh = ids ? static_cast<const void*>(st.h_hist_ids) : static_cast<const void*>(st.h_hist_emb);
+  const void* hc = ids ? static_cast<const void*>(st.h_cand_ids) : static_cast<const void*>(st.h_cand_emb);
+  CUDA_TRY(cudaSetDevice(e->ctx->device));
+  // only the slots in use cross PCIe (the kernels skip the others)
+  if (n * hrow > 0) CUDA_TRY(cudaMemcpyAsync(dh, hh, n * hrow, cudaMemcpyHostToDevice, s));
+  if (n * crow > 0) CUDA_TRY(cudaMemcpyAsync(dc, hc, n * crow, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(st.d_meta, st.h_meta, 4LL * e->R * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (e->graph_mode != mode || !e->graph_exec) {
+    const int rc = flame_exec_capture(e, mode, stream);
+    if (rc) return rc;
+  }
+  CUDA_TRY(cudaGraphLaunch(e->graph_exec, s));
+  if (n_score_rows > 0)
+    CUDA_TRY(cudaMemcpyAsync(st.h_scores, e->io.scores, n_score_rows * e->ctx->tasks * sizeof(float),
+                             cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaEventRecord(e->done_ev, s));
+  return 0;
+}
+
+int flame_exec_wait(FlameExec* e) {
+  if (!e || !e->done_ev) return fail(1, "nothing submitted");
+  CUDA_TRY(cudaEventSynchronize(e->done_ev));
+  return 0;
+}
+
+int flame_exec_query(FlameExec* e) {
+  if (!e || !e->done_ev) return 1;
+  const cudaError_t err = cudaEventQuery(e->done_ev);
+  if (err == cudaErrorNotReady) return 0;
+  if (err != cudaSuccess) return fail(2, std::string("exec query: ") + cudaGetErrorString(err));
+  return 1;
 }
 
 int flame_exec_profile(FlameExec* e, int mode, void* stream, int max_launches, float* ms,
