@@ -1208,9 +1208,6 @@ int flame_exec_submit(FlameExec* e, int mode, int n_req, long long n_score_rows,
     return fail(1, "batch exceeds executor capacity");
   const FlameStaging& st = e->stg;
   const bool ids = mode == FLAME_INPUT_IDS;
-  if (ids ? (!st.h_hist_ids || !st.h_cand_ids || !e->io.hist_ids || !e->io.cand_ids)
-          : (!st.h_hist_emb || !st.h_cand_emb || !e->io.hist_emb || !e->io.cand_emb))
-    return fail(1, "no staging buffers for this input mode");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const long long n = n_req;
   const long long hrow = ids ? e->H_bkt * 8LL : e->H_bkt * 4LL * e->ctx->d;
@@ -1221,6 +1218,8 @@ int flame_exec_submit(FlameExec* e, int mode, int n_req, long long n_score_rows,
                  : static_cast<void*>(const_cast<float*>(e->io.cand_emb));
   const void* hh = ids ? static_cast<const void*>(st.h_hist_ids) : static_cast<const void*>(st.h_hist_emb);
   const void* hc = ids ? static_cast<const void*>(st.h_cand_ids) : static_cast<const void*>(st.h_cand_emb);
+  if ((n * hrow > 0 && (!hh || !dh)) || (n * crow > 0 && (!hc || !dc)))
+    return fail(1, "no staging buffers for this input mode");
   CUDA_TRY(cudaSetDevice(e->ctx->device));
   // only the slots in use cross PCIe (the kernels skip the others)
   if (n * hrow > 0) CUDA_TRY(cudaMemcpyAsync(dh, hh, n * hrow, cudaMemcpyHostToDevice, s));
