@@ -288,7 +288,8 @@ class DeviceExecutor:
         one C call for the batch (flame_pack_padded)."""
         if not lens.any():
             return
-        parts = [a for a, l in zip(arrays, lens) if l]
+        # empty 2-D records may come as shape (0,): drop them (1-D id lists concatenate as they are)
+        parts = arrays if not width or lens.all() else [a for a, l in zip(arrays, lens.tolist()) if l]
         flat = np.concatenate(parts, dtype=dtype, casting="unsafe") if len(parts) > 1 \
             else np.asarray(parts[0], dtype=dtype)
         if width and (flat.ndim != 2 or flat.shape[1] != width):
@@ -467,8 +468,5 @@ class DeviceExecutor:
 
 
 def _split_rows(flat: np.ndarray, counts) -> list[np.ndarray]:
-    out, pos = [], 0
-    for c in counts:
-        out.append(flat[pos:pos + c])
-        pos += c
-    return out
+    ends = np.cumsum(counts).tolist()
+    return [flat[a:b] for a, b in zip([0] + ends[:-1], ends)]
