@@ -396,9 +396,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     // position p lives in buffer p & 1 and is loaded while position p - 2 is consumed
     uint8_t* rbuf = smem_resid + ew * C::kResidBytes;
     uint64_t* rfull = resid_full + 2 * ew;
-    auto nk_of = [&](int t) {
-      int gg, mp, nb;
-      decode(t, gg, mp, nb);
+    auto nk_of_nb = [&](int nb) {  // this warp's valid chunks of an n block
       int n = 0;
 #pragma unroll
       for (int k = 0; k < C::kMyChunks; ++k)
@@ -407,28 +405,36 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     };
     int ld_it = 0, ld_t = tile_at(0), ld_k = 0, ld_buf = 0, rd_buf = 0;
     uint32_t rd_phase = 0;  // bit b: parity of buffer b's next completion
+    // ld_t decoded once per tile (the divisions are not redone per residual box)
+    int ld_g = 0, ld_mb = 0, ld_nb = 0, ld_nk = 0;
+    auto ld_decode = [&]() {
+      if (ld_t >= total_tiles) return;
+      int mp;
+      decode(ld_t, ld_g, mp, ld_nb);
+      ld_mb = mp * ncl + crank;
+      ld_nk = nk_of_nb(ld_nb);
+    };
     auto ld_advance = [&](bool step) {
       if (step) ++ld_k;
-      while (ld_t < total_tiles && ld_k >= nk_of(ld_t)) {
+      while (ld_t < total_tiles && ld_k >= ld_nk) {
         ld_t = tile_at(++ld_it);
         ld_k = 0;
+        ld_decode();
       }
     };
     auto ld_issue = [&]() {
       if (ld_t >= total_tiles) return;
       if (epi_leader) {
-        int gg, mp, nb;
-        decode(ld_t, gg, mp, nb);
-        const int mb = mp * ncl + crank;
-        const int c0 = nb * BN + (half + ld_k * kEpiPerQuad) * 32;
-        const int r0 = min(mb * gemm::BM + wq * 32, ep.M - 1);
+        const int c0 = ld_nb * BN + (half + ld_k * kEpiPerQuad) * 32;
+        const int r0 = min(ld_mb * gemm::BM + wq * 32, ep.M - 1);
         ptx::mbar_arrive_expect_tx(&rfull[ld_buf], C::kResidBox);
-        ptx::tma_load_3d(rbuf + ld_buf * C::kResidBox, &tmR, &rfull[ld_buf], c0, r0, ep.resid_gstride ? gg : 0);
+        ptx::tma_load_3d(rbuf + ld_buf * C::kResidBox, &tmR, &rfull[ld_buf], c0, r0, ep.resid_gstride ? ld_g : 0);
       }
       ld_buf ^= 1;
       ld_advance(true);
     };
     if constexpr (C::kResidTma) {
+      ld_decode();
       ld_advance(false);
       ld_issue();
       ld_issue();
