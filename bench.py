@@ -31,6 +31,7 @@ the MAX over ranks.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import multiprocessing as mp
 import os
@@ -373,10 +374,11 @@ def run_ours(args, dist) -> None:
     from paper_2509_22681_b200.orchestrator import BucketScheduler
 
     sched = BucketScheduler(eng, target_rows=R * C, max_slots=R, with_ids=True)
-    e2e_steps = max(3, min(args.steps, 20))
+    e2e_steps = e2e_step_count(args, step_ms)
     for _ in sched.score_stream([reqs] * 2, ids=True):
         pass
     torch.cuda.synchronize()
+    gc.collect()
     dist.barrier()
     t0 = time.perf_counter()
     for _ in sched.score_stream([reqs] * e2e_steps, ids=True):
@@ -484,11 +486,12 @@ def run_dso(args, dist) -> None:
 
     # e2e through the scheduler's streaming API (async submit / collect over the
     # executor rings; the next batch is staged while the previous one runs)
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e_steps = e2e_step_count(args, step_ms)
     sched.executors_per_bucket = 3
     for _ in sched.score_stream([reqs] * 2, ids=True):
         pass
     torch.cuda.synchronize()
+    gc.collect()
     dist.barrier()
     t0 = time.perf_counter()
     for _ in sched.score_stream([reqs] * e2e_steps, ids=True):
@@ -528,6 +531,13 @@ def run_dso(args, dist) -> None:
               latency_note="p99_ms: per-request latency through BucketScheduler.score (one batch at a time: "
                            "call -> its group's scores on the host), nearest rank over e2e steps, max over ranks; "
                            "device step p99 in step_p99_ms")
+
+
+def e2e_step_count(args, step_ms) -> int:
+    """Batches in the e2e region: about 0.3 s of device work (at least --steps,
+    at most 400), so one host hiccup (a GC pass, a page fault) cannot swing it."""
+    per = max(1e-3, sum(step_ms) / len(step_ms)) / 1e3
+    return int(min(400, max(args.steps, 3, round(0.3 / per))))
 
 
 def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf, e2e_value, e2e_steps,

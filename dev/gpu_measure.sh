@@ -9,6 +9,9 @@ for w in cfg3 cfg4 cfg2 cfg5 cfg1 cfg3_l2; do
   timeout 900 python bench.py --workload $w --steps 20 --warmup 5 > $O/bench_$w.log 2>&1
   tail -1 $O/bench_$w.log > $O/bench_$w.json
 done
+# sustained: 150 back-to-back steps (the power cap shows after ~0.1 s of full load)
+timeout 900 python bench.py --workload cfg3 --steps 150 --warmup 5 --no-cpu-baseline > $O/bench_cfg3_sustained.log 2>&1
+tail -1 $O/bench_cfg3_sustained.log > $O/bench_cfg3_sustained.json
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/ref_cfg3.log 2>&1; tail -1 $O/ref_cfg3.log > $O/ref_cfg3.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 10 --csv \
   --log-file $O/launches_cfg3.csv python dev/prof_step.py cfg3 3 > $O/ncu_launch.log 2>&1
