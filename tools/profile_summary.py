@@ -93,5 +93,17 @@ all rows, with an fp32 residual stream. This row measures that path at full size
 * {d['e2e']['value'] / 1e6:.2f} M e2e;
 * {d['step_tflops']:.0f} TFLOP/s algorithmic.
 """
+su = P / "bench_cfg3_sustained.json"
+if su.exists():
+    d = json.loads(su.read_text())
+    s += f"""
+## Burst vs sustained (`bench_cfg3_sustained.json`)
+
+The cfg3 line above times 20 back-to-back steps (~45 ms). Timed over 150 steps
+(~0.35 s), the same pass gives {d['value'] / 1e6:.2f} M cand/s ({d['ms_per_step']:.3f} ms/step) at a median
+SM clock of {d['clocks']['sm_mhz']} MHz with throttle reasons {d['clocks']['reasons']}: under sustained
+full load the board's power cap takes the difference. The e2e figures are timed
+over ~0.3 s of device work and therefore show the sustained rate.
+"""
 (P / "SUMMARY.md").write_text(s)
 print(s[:1500])
