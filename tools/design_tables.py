@@ -28,11 +28,11 @@ new = (f"Results (`profiles/r01b/SUMMARY.md`), 1 × B200, SM clock {d3['clocks']
 s = s[:a] + new + s[b:]
 s = re.sub(r"One B200 does\n[0-9.]+ M, and the requests shard with no collective. The p99 request\n"
            r"latency is [0-9.]+ ms against a 20 ms target. End to end, from numpy ids to\n"
-           r"numpy scores through `BucketScheduler.score_stream`, cfg3 keeps\n[0-9]+ % of the device rate.",
+           r"numpy scores through `BucketScheduler.score_stream`, cfg3 keeps\n[0-9]+ % of the (?:20-step )?device rate.",
            f"One B200 does\n{d3['value'] / 1e6:.2f} M, and the requests shard with no collective. The p99 request\n"
            f"latency is {d3['p99_ms']:.2f} ms against a 20 ms target. End to end, from numpy ids to\n"
            f"numpy scores through `BucketScheduler.score_stream`, cfg3 keeps\n"
-           f"{100 * d3['e2e']['value'] / d3['value']:.0f} % of the device rate.", s)
+           f"{100 * d3['e2e']['value'] / d3['value']:.0f} % of the 20-step device rate.", s)
 s = re.sub(r"The measured step is [0-9.]+ ms, or\n[0-9]+ TFLOP/s\. That is [0-9]+ % of the measured sustained bf16 peak\n"
            r"\(1403 TF/s\) and [0-9]+ % of the burst peak \(1668 TF/s\)\.",
            f"The measured step is {d3['ms_per_step']:.3f} ms, or\n{d3['step_tflops']:.0f} TFLOP/s. That is "
