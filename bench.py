@@ -156,16 +156,24 @@ class ClockSampler:
         self._thread = threading.Thread(target=loop, daemon=True)
         self._thread.start()
 
+    def begin(self) -> None:
+        """The timed region starts now: earlier (idle) samples are not reported."""
+        self._begin = len(self.samples)
+
     def stop(self) -> dict:
         self._stop.set()
         if self._thread is not None:
             self._thread.join(timeout=2)
-        if not self.samples:
+        # samples from begin() to stop(); the last pre-begin sample if the region was shorter than a period
+        b = getattr(self, "_begin", 0)
+        samples = self.samples[b:] or self.samples[max(0, b - 1):b]
+        if not samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "samples": 0,
                     "reasons": [f"no samples: {self.error}"]}
-        reasons = sorted({n for _, rs in self.samples for n, bit in self.REASONS.items() if rs & bit})
-        return {"sm_mhz": statistics.median(sm for sm, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                "samples": len(self.samples), "reasons": reasons, "source": "NVML, 10 ms"}
+        reasons = sorted({n for _, rs in samples for n, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm for sm, _ in samples), "sm_min_mhz": min(sm for sm, _ in samples),
+                "sm_max_mhz": self.max_mhz, "samples": len(samples), "reasons": reasons,
+                "source": "NVML, 10 ms, timed region only"}
 
 
 # ------------------------------------------------------------- CPU oracle
@@ -350,6 +358,7 @@ def run_ours(args, dist) -> None:
     clocks = ClockSampler(dev.index)
     clocks.start()
     time.sleep(0.3)
+    clocks.begin()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with torch.cuda.stream(ex.stream):
         evs[0].record(ex.stream)
@@ -474,6 +483,7 @@ def run_dso(args, dist) -> None:
     clocks = ClockSampler(dev.index)
     clocks.start()
     time.sleep(0.3)
+    clocks.begin()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for a, b in evs:
         step(a, b)
