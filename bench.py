@@ -572,6 +572,7 @@ def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99
             "step_tflops": round(step_tf, 1),
             "e2e": {"value": e2e_value, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "timing": "host wall clock over ~0.3 s of device work (sustained, power-capped rate)",
                     "path": e2e_path or ("BucketScheduler.score_stream(ids=True): numpy ids -> pinned -> H2D -> "
                                          "graph -> D2H -> numpy, one step in flight ahead")},
             "gpu_launches": launches * args.steps,
