@@ -27,7 +27,8 @@ ref = json.loads((P / "reference_arm_cfg3.json").read_text())
 d3 = json.loads((P / "bench_cfg3.json").read_text())
 s = f"""# Round 1 measurements — 1 × B200
 
-Every number here comes from one `gpurun` call of `dev/gpu_measure.sh`. The call ran:
+The tables come from one `gpurun` call of `dev/gpu_measure.sh` (the burst-vs-sustained
+section at the end from a second call on one box). The call ran:
 * the GPU parity tests (all pass);
 * `smoke()`;
 * `tools/parity_report.py`;
