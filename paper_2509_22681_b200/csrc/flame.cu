@@ -59,13 +59,12 @@ cudaError_t launch_dedup_t(const PdaLists& l, int lists, cudaStream_t s) {
   constexpr size_t kSort = sizeof(typename Sort::TempStorage);
   constexpr size_t kArrays = static_cast<size_t>(kThreads) * kItems * 16;
   constexpr size_t kSmem = kSort > kArrays ? kSort : kArrays;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(pda_dedup<kThreads, kItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static DeviceOnce once;
+  cudaError_t e = once.run([](int) {
+    return cudaFuncSetAttribute(pda_dedup<kThreads, kItems>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmem));
+  });
+  if (e != cudaSuccess) return e;
   pda_dedup<kThreads, kItems><<<lists, kThreads, kSmem, s>>>(l);
   return cudaGetLastError();
 }
@@ -121,6 +120,7 @@ struct FlameCtx {
   void* table = nullptr;
   long long num_items = 0;
   int table_dtype = FLAME_TABLE_FP32;
+  unsigned table_gen = 0;  // bumped when the table buffer / size / dtype changes (captured graphs bake them in)
   std::vector<void*> allocs;
 
   ~FlameCtx() {
@@ -170,6 +170,7 @@ struct FlameExec {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   int graph_mode = -1;
+  unsigned graph_table_gen = 0;  // table generation the captured graph was built against
   int launches = 0;
   std::vector<void*> allocs;
   FlameStaging stg{};
@@ -575,12 +576,15 @@ struct Pipe {
       if (!make_tmap_bf16_3d(&tm, e->QKV, 3ULL * c->DA, e->rows, c->G, 3ULL * c->DA * 2,
                              e->rows * 3ULL * c->DA * 2, 64, 128))
         return fail(2, "tensor map for QKV failed");
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(sumi_attention_tcgen05<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes);
-        cudaFuncSetAttribute(sumi_attention_tcgen05<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes);
-        attr = true;
-      }
+      static DeviceOnce once;
+      cudaError_t ae = once.run([](int) {
+        cudaError_t e = cudaFuncSetAttribute(sumi_attention_tcgen05<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             attn::kSmemBytes);
+        if (e != cudaSuccess) return e;
+        return cudaFuncSetAttribute(sumi_attention_tcgen05<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    attn::kSmemBytes);
+      });
+      if (ae != cudaSuccess) return fail(2, std::string("attention attributes: ") + cudaGetErrorString(ae));
       a.nh = c->nh;
       const int units = e->R * c->G * c->nh;  // persistent: one CTA per SM walks the units
       dim3 tgrid(units < c->num_sms ? units : c->num_sms);
@@ -966,25 +970,37 @@ int flame_set_table(FlameCtx* c, const float* host_table, long long num_items, i
   if (dtype != FLAME_TABLE_BF16 && dtype != FLAME_TABLE_FP32) return fail(1, "bad table dtype");
   CUDA_TRY(cudaSetDevice(c->device));
   const size_t n = static_cast<size_t>(num_items) * c->D;
-  void* dev = nullptr;
+  const size_t esz = dtype == FLAME_TABLE_BF16 ? 2 : 4;
+  std::vector<unsigned char> host(n * esz + 16, 0);
   if (dtype == FLAME_TABLE_BF16) {
-    std::vector<__nv_bfloat16> t(n, __float2bfloat16_rn(0.f));
+    __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(host.data());
     for (long long i = 0; i < num_items; ++i)
       for (int k = 0; k < c->d; ++k) t[static_cast<size_t>(i) * c->D + k] = __float2bfloat16_rn(host_table[static_cast<size_t>(i) * c->d + k]);
-    dev = c->alloc<__nv_bfloat16>(n);
-    if (!dev) return fail(2, "table allocation failed");
-    CUDA_TRY(cudaMemcpy(dev, t.data(), n * 2, cudaMemcpyHostToDevice));
   } else {
-    std::vector<float> t(n, 0.f);
+    float* t = reinterpret_cast<float*>(host.data());
     for (long long i = 0; i < num_items; ++i)
       for (int k = 0; k < c->d; ++k) t[static_cast<size_t>(i) * c->D + k] = host_table[static_cast<size_t>(i) * c->d + k];
-    dev = c->alloc<float>(n);
-    if (!dev) return fail(2, "table allocation failed");
-    CUDA_TRY(cudaMemcpy(dev, t.data(), n * 4, cudaMemcpyHostToDevice));
+  }
+  if (c->table && num_items == c->num_items && dtype == c->table_dtype) {
+    // same shape and dtype: overwrite in place, so captured graphs stay valid
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(c->table, host.data(), n * esz, cudaMemcpyHostToDevice));
+    return 0;
+  }
+  void* dev = dtype == FLAME_TABLE_BF16 ? static_cast<void*>(c->alloc<__nv_bfloat16>(n)) : static_cast<void*>(c->alloc<float>(n));
+  if (!dev) return fail(2, "table allocation failed");
+  CUDA_TRY(cudaMemcpy(dev, host.data(), n * esz, cudaMemcpyHostToDevice));
+  if (c->table) {
+    // the old buffer may still be read by queued work: drain, then free it; executors
+    // re-capture their graphs against the new table (table_gen) before the next replay
+    CUDA_TRY(cudaDeviceSynchronize());
+    for (auto it = c->allocs.begin(); it != c->allocs.end(); ++it)
+      if (*it == c->table) { cudaFree(*it); c->allocs.erase(it); break; }
   }
   c->table = dev;
   c->num_items = num_items;
   c->table_dtype = dtype;
+  ++c->table_gen;
   return 0;
 }
 
@@ -1174,6 +1190,7 @@ int flame_exec_capture(FlameExec* e, int mode, void* stream) {
         err = cudaGraphInstantiate(&e->graph_exec, g, 0);
         if (err != cudaSuccess) rc = fail(2, std::string("graph instantiate: ") + cudaGetErrorString(err));
         e->graph_mode = mode;
+        e->graph_table_gen = e->ctx->table_gen;
         e->launches = n;
       } else if (g) {
         cudaGraphDestroy(g);
@@ -1189,6 +1206,9 @@ int flame_exec_capture(FlameExec* e, int mode, void* stream) {
 
 int flame_exec_replay(FlameExec* e, void* stream) {
   if (!e || !e->graph_exec) return fail(1, "executor has no captured graph");
+  if (e->graph_table_gen != e->ctx->table_gen) {  // the item table was replaced since capture
+    if (int rc = flame_exec_capture(e, e->graph_mode, stream)) return rc;
+  }
   CUDA_TRY(cudaGraphLaunch(e->graph_exec, static_cast<cudaStream_t>(stream)));
   return 0;
 }
@@ -1225,7 +1245,7 @@ int flame_exec_submit(FlameExec* e, int mode, int n_req, long long n_score_rows,
   if (n * hrow > 0) CUDA_TRY(cudaMemcpyAsync(dh, hh, n * hrow, cudaMemcpyHostToDevice, s));
   if (n * crow > 0) CUDA_TRY(cudaMemcpyAsync(dc, hc, n * crow, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(st.d_meta, st.h_meta, 4LL * e->R * sizeof(int), cudaMemcpyHostToDevice, s));
-  if (e->graph_mode != mode || !e->graph_exec) {
+  if (e->graph_mode != mode || !e->graph_exec || e->graph_table_gen != e->ctx->table_gen) {
     const int rc = flame_exec_capture(e, mode, stream);
     if (rc) return rc;
   }

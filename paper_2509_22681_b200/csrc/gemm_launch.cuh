@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include "gemm_tcgen05.cuh"
 #include "tmap.cuh"
+#include "device_once.cuh"
 
 namespace flame {
 
@@ -34,9 +35,9 @@ template <int BN, int EPI>
 static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_sms) {
   using C1 = gemm::Cfg<BN, EPI, 1>;
   using C = gemm::Cfg<BN, EPI, 2>;
-  static bool attr_set = false;
-  static int max_clusters = 0;  // co-resident CTA pairs at this smem size
-  if (!attr_set) {
+  static DeviceOnce once;
+  static int max_clusters_dev[kMaxDevices];  // co-resident CTA pairs at this smem size, per device
+  cudaError_t setup = once.run([&](int dev) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, EPI, 1>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C1::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -54,12 +55,16 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
     q.dynamicSmemBytes = C::kSmemBytes;
     q.attrs = at;
     q.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, gemm_bf16_tcgen05<BN, EPI, 2>, &q) != cudaSuccess) {
+    int mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, gemm_bf16_tcgen05<BN, EPI, 2>, &q) != cudaSuccess) {
       cudaGetLastError();
-      max_clusters = 0;
+      mc = 0;
     }
-    attr_set = true;
-  }
+    max_clusters_dev[dev] = mc;
+    return cudaSuccess;
+  });
+  if (setup != cudaSuccess) return setup;
+  const int max_clusters = max_clusters_dev[current_device()];
   const int m_tiles = (p.M + gemm::BM - 1) / gemm::BM;
   const int n_tiles = (p.N + BN - 1) / BN;
   // CTA pairs halve each CTA's W-tile traffic from L2, which is what paces the

@@ -423,9 +423,12 @@ class DeviceExecutor:
     def collect(self) -> list[np.ndarray]:
         if self._pending is None:
             raise RuntimeError("nothing submitted")
-        self.wait()
-        counts, self._pending = self._pending, None
-        flat = self.h_scores[: self.n_real].numpy().astype(np.float64)
+        counts = self._pending
+        try:
+            self.wait()
+            flat = self.h_scores[: self.n_real].numpy().astype(np.float64)
+        finally:
+            self._pending = None  # a failed batch must not leave the executor stuck
         return _split_rows(flat, counts)
 
     def profile(self, mode: int = _lib.INPUT_EMBEDDINGS, max_launches: int = 256) -> list[dict]:

@@ -14,9 +14,11 @@ replay per shape group.
 Names, validation and errors follow the reference: ``ScoreRequest`` /
 ``ScoreResponse``, ``RequestError(ValueError)`` (HTTP 400) for contract
 violations (``service.py:115-125``), ``ServiceClosedError(RuntimeError)`` (503)
-after ``close``.  Unknown ids (outside the table) score as zero embeddings, as
-an empty store value does in the reference (``decode_embedding``,
-``store.py:74-78``).  ``mutate`` mirrors ``SimulatedRemoteStore.mutate``
+after ``close``.  The reference store resolves every id deterministically
+(``item_embedding``, ``store.py:59-63``), so a request holding ids outside the
+device table (negative, or >= ``num_items``) is resolved on the host with the
+same store function and scored through the embedding path; its scores equal
+what the reference serves for those ids.  ``mutate`` mirrors ``SimulatedRemoteStore.mutate``
 (``store.py:104-108``): the key's version advances and its row is refreshed in
 HBM at once (the incremental-refresh path of SURVEY §8f.2), so later requests
 see the new features.
@@ -317,52 +319,73 @@ class DeviceService:
                         self._cv.notify_all()
 
     def _host_rows(self, ids: np.ndarray) -> np.ndarray:
-        """The store's rows for ``ids`` (zeros for unknown ids), resolved on the host."""
+        """The store's rows for ``ids``, resolved on the host: table ids from the
+        store copy, any other id from the store function (store.py:59-63)."""
         rows = np.zeros((ids.size, self.config.hidden_dim), dtype=np.float32)
         ok = (ids >= 0) & (ids < self.num_items)
         rows[ok] = self._store[ids[ok]]
+        for k in np.flatnonzero(~ok):
+            rows[k] = self.embedding_of(int(ids[k]))
         return rows
+
+    def _in_table(self, t) -> bool:
+        n = self.num_items
+        return bool((t.hist.size == 0 or (t.hist.min() >= 0 and t.hist.max() < n))
+                    and (t.cand.min() >= 0 and t.cand.max() < n))
 
     def _submit(self, batch):
         """Resolve the batch's features and submit it (explicit routing), or run
-        it to completion (implicit routing).  Returns what ``_complete`` needs."""
+        it to completion (implicit routing).  Returns what ``_complete`` needs.
+        With the cache on, requests whose ids all lie in the device table go as
+        id lists (PDA on the device); the others are resolved on the host."""
         d = self.config.hidden_dim
         n_ids = sum(t.hist.size + t.cand.size for t in batch)
-        if self.cache_enabled:
-            hits = sum(int(np.count_nonzero((t.hist >= 0) & (t.hist < self.num_items)))
-                       + int(np.count_nonzero((t.cand >= 0) & (t.cand < self.num_items))) for t in batch)
-            work = [(t.hist, t.cand) for t in batch]
-            nbytes = 8 * n_ids
-        else:
-            hits = 0
-            work = [(self._host_rows(t.hist), self._host_rows(t.cand)) for t in batch]
-            nbytes = 4 * d * n_ids
+        on_dev = [self.cache_enabled and self._in_table(t) for t in batch]
+        id_work = [(t.hist, t.cand) for t, f in zip(batch, on_dev) if f]
+        row_work = [(self._host_rows(t.hist), self._host_rows(t.cand)) for t, f in zip(batch, on_dev) if not f]
+        hits = sum(t.hist.size + t.cand.size for t, f in zip(batch, on_dev) if f)
+        nbytes = 8 * hits + 4 * d * (n_ids - hits)
         with self._stats_lock:
             self.dispatches += 1
             self.lookups += n_ids
             self.hits += hits
             self.feature_bytes += nbytes
+        order = [i for i, f in enumerate(on_dev) if f] + [i for i, f in enumerate(on_dev) if not f]
         with self._lock:
             if self.routing == "explicit":
-                rec = self.scheduler.submit_batch(work, ids=self.cache_enabled)
-                with self._cv:
-                    self._on_device += 1
-                return ("rec", rec)
-            return ("done", [self._run_implicit(h, c) for h, c in work])
+                recs = []
+                for work, ids in ((id_work, True), (row_work, False)):
+                    if work:
+                        recs.append(self.scheduler.submit_batch(work, ids=ids))
+                        with self._cv:
+                            self._on_device += 1
+                return ("rec", (order, recs))
+            out = [self._run_implicit(h, c, True) for h, c in id_work]
+            out += [self._run_implicit(h, c, False) for h, c in row_work]
+            return ("done", (order, out))
 
     def _complete(self, batch, handle) -> None:
-        kind, obj = handle
+        kind, (order, obj) = handle
+        scores, lat = [], []
         if kind == "rec":
-            try:
-                scores, lat = self.scheduler.collect_batch(obj)
-            finally:
-                with self._cv:
-                    self._on_device -= 1
-                    self._cv.notify_all()
+            err = None
+            for rec in obj:
+                try:
+                    s_, l_ = self.scheduler.collect_batch(rec)
+                    scores += s_
+                    lat += l_
+                except BaseException as exc:  # noqa: BLE001 - every rec is collected first
+                    err = err or exc
+                finally:
+                    with self._cv:
+                        self._on_device -= 1
+                        self._cv.notify_all()
+            if err is not None:
+                raise err
         else:
             scores, lat = [s for s, _ in obj], [l for _, l in obj]
-        for t, s, l in zip(batch, scores, lat):
-            t.scores, t.lat = s, l
+        for i, s_, l_ in zip(order, scores, lat):
+            batch[i].scores, batch[i].lat = s_, l_
 
     def _quiesce(self) -> None:
         """Wait until no batch is on the device (caller holds ``_lock``, so no
@@ -370,15 +393,15 @@ class DeviceService:
         with self._cv:
             self._cv.wait_for(lambda: self._on_device == 0)
 
-    def _run_implicit(self, hist, cand):
+    def _run_implicit(self, hist, cand, ids: bool):
         """Reference ImplicitShapeRunner (orchestrator.py:225-260): exact-shape
         buffers allocated for the request, eager launch, released afterwards."""
         ex = DeviceExecutor(self.engine, 1, len(hist) // self.config.num_blocks, len(cand),
-                            with_ids=self.cache_enabled, pinned=self.mem_opt)
+                            with_ids=ids, pinned=self.mem_opt)
         self._implicit_allocs += ex.allocations
         try:
             t0 = time.perf_counter()
-            if self.cache_enabled:
+            if ids:
                 s = ex.score_ids([(hist, cand)], graph=False)[0]
             else:
                 s = ex.score([(hist, cand)], graph=False)[0]
@@ -395,25 +418,28 @@ class DeviceService:
     # -- feature path ---------------------------------------------------------
 
     def embedding_of(self, item_id: int) -> np.ndarray:
-        """The store's current embedding of an item (zeros outside the table)."""
-        if not 0 <= item_id < self.num_items:
-            return np.zeros(self.config.hidden_dim)
+        """The store's current embedding of an item (store.py:59-63, any id)."""
         return item_embedding(self.store_seed, int(item_id), self._versions.get(int(item_id), 0),
                               self.config.hidden_dim)
 
     def mutate(self, item_ids) -> None:
         """Advance the items' versions (reference store.mutate) and refresh their
-        rows in the device table."""
-        ids = [int(i) for i in np.atleast_1d(item_ids) if 0 <= int(i) < self.num_items]
+        rows in the device table.  The version bump, the row computation and the
+        device update happen under one lock, so concurrent mutates of one id
+        cannot leave the table behind ``_versions``."""
+        ids = [int(i) for i in np.atleast_1d(item_ids)]
         if not ids:
             return
-        for i in ids:
-            self._versions[i] = self._versions.get(i, 0) + 1
-        rows = np.stack([self.embedding_of(i) for i in ids])
         with self._lock:
+            for i in ids:
+                self._versions[i] = self._versions.get(i, 0) + 1
+            tab = sorted({i for i in ids if 0 <= i < self.num_items})
+            if not tab:
+                return
+            rows = np.stack([self.embedding_of(i) for i in tab])
             self._quiesce()
-            self._store[ids] = rows
-            self.engine.update_rows(np.asarray(ids, dtype=np.int64), rows)
+            self._store[tab] = rows
+            self.engine.update_rows(np.asarray(tab, dtype=np.int64), rows)
         with self._stats_lock:
             self.feature_bytes += rows.size * 4
 

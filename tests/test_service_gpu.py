@@ -21,10 +21,10 @@ def request_of(hist, cand):
 
 
 def resolve(ids, versions=None):
-    """Reference resolve_embeddings (service.py:97-108) over the store function."""
+    """Reference resolve_embeddings (service.py:97-108) over the store function
+    (store.py:59-63 resolves every id, in the table or not)."""
     versions = versions or {}
-    rows = [item_embedding(1234, int(i), versions.get(int(i), 0), CFG.hidden_dim) if 0 <= i < NUM_ITEMS
-            else np.zeros(CFG.hidden_dim) for i in ids]
+    rows = [item_embedding(1234, int(i), versions.get(int(i), 0), CFG.hidden_dim) for i in ids]
     return np.asarray(rows).reshape(len(ids), CFG.hidden_dim)
 
 
@@ -52,7 +52,8 @@ def test_identical_requests_identical_scores(service):
     np.testing.assert_array_equal(service.handle_request(req).scores, service.handle_request(req).scores)
 
 
-def test_batch_equals_single_and_unknown_ids_are_zero_rows(service):
+def test_batch_equals_single_and_ids_outside_the_table_resolve_like_the_store(service):
+    # ids < 0 or >= num_items: host-resolved with the store function
     rng = np.random.default_rng(3)
     reqs = [request_of(rng.integers(-5, NUM_ITEMS + 50, 2 * int(rng.integers(0, 33))),
                        rng.integers(-5, NUM_ITEMS + 50, int(rng.integers(1, 33)))) for _ in range(12)]
@@ -66,10 +67,14 @@ def test_batch_equals_single_and_unknown_ids_are_zero_rows(service):
 def test_mutate_refreshes_device_rows(service):
     req = request_of(range(8), range(100, 104))
     before = service.handle_request(req).scores
-    service.mutate([101, 3])
+    service.mutate([101, 3, NUM_ITEMS + 7])
     after = service.handle_request(req).scores
     assert not np.array_equal(before, after)
-    versions = {101: 1, 3: 1}
+    versions = {101: 1, 3: 1, NUM_ITEMS + 7: 1}
+    req2 = request_of(range(8), [NUM_ITEMS + 7])
+    want2 = orc.model_forward(resolve(req2.history_item_ids, versions), resolve(req2.candidate_item_ids, versions),
+                              service.params, CFG)
+    assert np.abs(service.handle_request(req2).scores - want2).max() <= 2e-2
     want = orc.model_forward(resolve(req.history_item_ids, versions), resolve(req.candidate_item_ids, versions),
                              service.params, CFG)
     assert np.abs(after - want).max() <= 2e-2
