@@ -43,28 +43,47 @@ def _require_cuda(device) -> torch.device:
 class FlameEngine:
     """One device context: repacked weights (+ optional embedding table)."""
 
-    def __init__(self, params: ModelParams, config: ModelConfig, precision: str = "bf16",
-                 device=None) -> None:
+    def __init__(self, params: ModelParams | None, config: ModelConfig, precision: str = "bf16",
+                 device=None, *, flmp: bytes | None = None) -> None:
+        if params is None and flmp is None:
+            raise ValueError("params or an FLMP image is required")
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {tuple(PRECISIONS)}, got {precision!r}")
         self.lib = _lib.load()
         self.device = _require_cuda(device)
         self.config = config
         self.precision = precision
-        desc = _lib.FlameModelDesc(
-            config.hidden_dim, config.head_dim, config.num_blocks, config.layers_per_block,
-            config.ffn_dim, config.num_tasks, config.max_history_len, config.max_candidates,
-            config.seed)
-        stream = np.ascontiguousarray(param_stream(params), dtype=np.float64)
         ctx = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            _lib.check(self.lib.flame_create(ctypes.byref(desc), stream.ctypes.data, stream.size,
-                                             PRECISIONS[precision], self.device.index,
-                                             ctypes.byref(ctx)))
+            if flmp is not None:
+                # the C loader parses the FLMP header and body itself (flame_create_flmp)
+                buf = np.frombuffer(flmp, dtype=np.uint8)
+                _lib.check(self.lib.flame_create_flmp(buf.ctypes.data, buf.size, PRECISIONS[precision],
+                                                      self.device.index, ctypes.byref(ctx)))
+            else:
+                desc = _lib.FlameModelDesc(
+                    config.hidden_dim, config.head_dim, config.num_blocks, config.layers_per_block,
+                    config.ffn_dim, config.num_tasks, config.max_history_len, config.max_candidates,
+                    config.seed)
+                stream = np.ascontiguousarray(param_stream(params), dtype=np.float64)
+                _lib.check(self.lib.flame_create(ctypes.byref(desc), stream.ctypes.data, stream.size,
+                                                 PRECISIONS[precision], self.device.index,
+                                                 ctypes.byref(ctx)))
         self._ctx = ctx
         self._executors: dict[tuple, "DeviceExecutor"] = {}
         self._lock = threading.Lock()
         self.num_items = 0
+
+    @classmethod
+    def from_flmp(cls, source, precision: str = "bf16", device=None) -> "FlameEngine":
+        """Device context straight from an FLMP parameter file (path or bytes,
+        reference model/params.py:131-207): the C library parses the header and
+        repacks the fp64 body; the host only reads the config for its own use."""
+        from .params import config_from_header
+
+        data = bytes(source) if isinstance(source, (bytes, bytearray, memoryview)) else open(source, "rb").read()
+        config = config_from_header(data)
+        return cls(None, config, precision=precision, device=device, flmp=data)
 
     @property
     def handle(self) -> ctypes.c_void_p:

@@ -63,3 +63,40 @@ def test_package_flop_formula_matches_oracle_formula():
     for dims, H, C in [((64, 16, 2, 2, 256, 2, 256, 64), 256, 64), ((512, 64, 8, 1, 2048, 2, 2048, 512), 2048, 512)]:
         cfg = fb.ModelConfig(*dims)
         assert algorithmic_flops(cfg, H, C) == orc.algorithmic_flops(cfg, H, C)
+
+
+@pytest.mark.parametrize("name", ["cfg4_c16", "cfg4_c2048"])
+def test_oracle_cfg4_candidate_range_ends(name):
+    # round-2 fixtures (oracle/gen_golden_r2.py): both ends of the DSO candidate range
+    cfg, params, hist, cand, blob = golden_forward(name)
+    assert np.abs(orc.model_forward(hist, cand, params, cfg) - blob["scores"]).max() <= 1e-12
+
+
+def test_oracle_bench_id_path_first_request():
+    """The oracle's resolve + forward on the first request of bench.py's cfg3 batch
+    (Zipf ids over 100k items) equals the reference Service + model_forward."""
+    import paper_2509_22681_b200 as fb
+
+    g = load_golden("ids_cfg3.npz")
+    dims = [int(x) for x in g["dims"]]
+    cfg = fb.ModelConfig(*dims[:8], seed=dims[8])
+    h, c = g["hist_ids"][0], g["cand_ids"][0]
+    ids = np.union1d(h, c)
+    table = np.zeros((int(ids.max()) + 1, cfg.hidden_dim))
+    for i in ids:
+        table[i] = orc.item_embedding(int(g["store_seed"]), int(i), 0, cfg.hidden_dim)
+    hist, _, _ = orc.resolve_embeddings(h, table)
+    cand, _, _ = orc.resolve_embeddings(c, table)
+    out = orc.model_forward(hist, cand, fb.init_params(cfg), cfg)
+    assert np.abs(out - g["scores"][0]).max() <= 1e-12
+
+
+def test_bench_generator_reproduces_fixture_ids():
+    """bench.make_requests draws the same ids as the reference _KeySampler did for the fixture."""
+    import bench
+
+    g = load_golden("ids_cfg3.npz")
+    reqs = bench.make_requests(8, 2048, 512, int(g["workload_seed"]))
+    for (h, c), hh, cc in zip(reqs, g["hist_ids"], g["cand_ids"]):
+        np.testing.assert_array_equal(h, hh)
+        np.testing.assert_array_equal(c, cc)
