@@ -274,10 +274,45 @@ def _cpu_name() -> str:
     return "unknown CPU"
 
 
-def roofline(prof_runs: list, name: str):
+def choose_peak(tensor: bool, clk: dict | None) -> tuple[float, str]:
+    """Roofline denominator for a kernel timed under the clocks ``clk`` (the
+    profile pass's own NVML record): the burst bf16 figure when the SM clock sat
+    at its maximum with no power cap, the sustained one otherwise; HBM: the
+    measured copy bandwidth."""
+    peaks, src = load_peaks()
+    if not tensor:
+        return peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]), f"{src} (hbm_gbs)"
+    burst = bool(clk and clk.get("sm_mhz") and clk.get("sm_max_mhz")
+                 and clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"] and "sw_power_cap" not in clk.get("reasons", []))
+    key = "bf16_tflops" if burst else "bf16_tflops_sustained"
+    why = "profile-pass SM clock at max, no power cap" if burst else "profile-pass SM clock below max or power-capped"
+    return peaks.get(key, FALLBACK_PEAKS[key]), f"{src} ({key}: {why})"
+
+
+def pda_algorithmic_bytes(ex, d: int, table_bytes: int) -> dict:
+    """SURVEY §8(d) PDA bytes of the executor's last id pass, from the unique-id
+    counts the dedup kernel wrote (n_unique): dedup = ids in + unique ids and
+    inverse out; gather = one table row per UNIQUE id + the assembled rows
+    (centered bf16 for every position, + the fp32 residual copy of candidates)."""
+    import torch
+
+    torch.cuda.synchronize()
+    nu = ex.n_unique.cpu().numpy().astype(np.int64)
+    R = ex.R
+    meta = ex.meta.cpu().numpy().astype(np.int64)
+    n = int(meta[3, 0])  # active slots (the dedup kernel skips the others)
+    hl, cl = meta[0, :n], meta[1, :n]
+    n_pos = int(hl.sum() + cl.sum())
+    n_uniq = int(nu[:n].sum() + nu[R:R + n].sum())
+    dedup = 8 * n_pos + 8 * n_uniq + 8 * n_pos
+    gather = n_uniq * d * table_bytes + n_pos * d * 2 + int(cl.sum()) * d * 4
+    return {"pda_dedup": float(dedup), "pda_gather": float(gather), "unique_rows": n_uniq, "positions": n_pos}
+
+
+def roofline(prof_runs: list, name: str, prof_clk: dict | None = None, byte_override: dict | None = None):
     """Aggregate per-launch profiles ([[{name, ms, flops, bytes}]] of eager runs)
-    into per-kernel figures and the dominant kernel's roofline point."""
-    peaks, peak_src = load_peaks()
+    into per-kernel figures and the dominant kernel's roofline point.  The peak
+    follows the profile pass's own clock record (``choose_peak``)."""
     n_runs = len(prof_runs)
     agg: dict = {}
     for run in prof_runs:
@@ -286,7 +321,7 @@ def roofline(prof_runs: list, name: str):
             a["ms"] += rec["ms"]
             a["n"] += 1
             a["flops"] += rec["flops"]
-            a["bytes"] += rec["bytes"]
+            a["bytes"] += (byte_override or {}).get(rec["name"], rec["bytes"])
     step_prof_ms = sum(a["ms"] for a in agg.values()) / n_runs
     top = max(agg, key=lambda k: agg[k]["ms"])
     t = agg[top]
@@ -294,8 +329,9 @@ def roofline(prof_runs: list, name: str):
     tensor = t["flops"] > 0
     per_launch = (t["flops"] if tensor else t["bytes"]) / t["n"]
     achieved = per_launch / (avg_ms / 1e3) / (1e12 if tensor else 1e9)
-    peak = peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]) if tensor \
-        else peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+    peak, peak_src = choose_peak(tensor, prof_clk)
+    peak_t, _ = choose_peak(True, prof_clk)
+    peak_b, _ = choose_peak(False, prof_clk)
     traffic = None
     ncu = ROOT / "profiles" / "ncu_dram_per_launch.json"
     if ncu.exists():
@@ -303,12 +339,24 @@ def roofline(prof_runs: list, name: str):
             traffic = json.loads(ncu.read_text()).get(name, {}).get(top)
         except Exception:
             traffic = None
-    kernels = {k: {"ms_per_step": round(v["ms"] / n_runs, 4),
-                   "share": round(v["ms"] / n_runs / step_prof_ms, 4),
-                   "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) if v["flops"] else None,
-                   "gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)}
-               for k, v in sorted(agg.items(), key=lambda kv: -kv[1]["ms"])}
+    kernels = {}
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1]["ms"]):
+        tf = v["flops"] / (v["ms"] / 1e3) / 1e12 if v["flops"] else None
+        gb = v["bytes"] / (v["ms"] / 1e3) / 1e9
+        kernels[k] = {"ms_per_step": round(v["ms"] / n_runs, 4), "share": round(v["ms"] / n_runs / step_prof_ms, 4),
+                      "tflops": round(tf, 1) if tf is not None else None, "gbs": round(gb, 1),
+                      "frac": round(tf / peak_t, 4) if tf is not None else round(gb / peak_b, 4)}
     return tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels
+
+
+def profile_pass(ex, mode, runs: int, dev_index: int):
+    """Per-launch CUDA-event profile of ``runs`` eager passes with its own NVML
+    clock record (the roofline's peak is chosen from these clocks)."""
+    clocks = ClockSampler(dev_index, period_s=0.002)
+    clocks.start()
+    clocks.begin()
+    prof = [ex.profile(mode) for _ in range(runs)]
+    return prof, clocks.stop()
 
 
 def cpu_baseline_line(args, dist, name: str):
@@ -376,6 +424,14 @@ def run_ours(args, dist) -> None:
     cands = R * C * args.steps * dist.world_size
     value = cands / (total_ms / 1e3)
 
+    # --------------------------------------------------- roofline (live)
+    # eager per-launch CUDA events, before the long e2e region (so its clocks are
+    # not the power-capped tail of it), with its own clock record
+    prof, prof_clk = profile_pass(ex, _lib.INPUT_IDS, 5, dev.index)
+    pda = pda_algorithmic_bytes(ex, d, 4)
+    tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels = roofline(
+        prof, name, prof_clk, {k: pda[k] for k in ("pda_dedup", "pda_gather")})
+
     # -------------------------------------------------------------- e2e
     # through the public streaming API: numpy ids in, numpy scores out, every step
     # staged into pinned buffers, copied H2D, replayed, copied D2H; consecutive
@@ -390,16 +446,19 @@ def run_ours(args, dist) -> None:
     gc.collect()
     dist.barrier()
     t0 = time.perf_counter()
+    req_lat = []
     for _ in sched.score_stream([reqs] * e2e_steps, ids=True):
-        pass
+        req_lat += sched.last_latencies
     e2e_s = dist.max(time.perf_counter() - t0)
     e2e_value = R * C * e2e_steps * dist.world_size / e2e_s
+    # per-request latency end to end: from the submission of the request's batch
+    # (numpy ids on the host) to its scores back on the host, in the streaming
+    # (throughput) mode, i.e. including the wait behind the batch in flight ahead
+    e2e_p99 = dist.max(1000 * nearest_rank(req_lat, 0.99))
+    e2e_p50 = dist.max(1000 * nearest_rank(req_lat, 0.5))
     h2d = R * (nb * (H // nb) + C) * 8 + 3 * R * 4
     d2h = R * C * tasks * 4
 
-    # --------------------------------------------------- roofline (live)
-    prof = [ex.profile(_lib.INPUT_IDS) for _ in range(3)]
-    tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels = roofline(prof, name)
     from paper_2509_22681_b200.flops import algorithmic_flops
 
     step_flops = algorithmic_flops(cfg, H, C) * R
@@ -410,7 +469,7 @@ def run_ours(args, dist) -> None:
 
     emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf, e2e_value, e2e_steps,
               h2d, d2h, launches, tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels, clk,
-              cpu_baseline)
+              cpu_baseline, prof_clk=prof_clk, pda=pda, e2e_lat=(e2e_p50, e2e_p99))
 
 
 def run_dso(args, dist) -> None:
@@ -494,6 +553,16 @@ def run_dso(args, dist) -> None:
     total_ms = dist.max(sum(step_ms))
     value = n_cand * args.steps * dist.world_size / (total_ms / 1e3)
 
+    clocks_p = ClockSampler(dev.index, period_s=0.002)
+    clocks_p.start()
+    clocks_p.begin()
+    prof = [[rec for ex in groups for rec in ex.profile(_lib.INPUT_IDS)] for _ in range(2)]
+    prof_clk = clocks_p.stop()
+    pdas = [pda_algorithmic_bytes(ex, d, 4) for ex in groups]
+    pda = {k: sum(p[k] for p in pdas) for k in pdas[0]}
+    tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels = roofline(
+        prof, name, prof_clk, {k: pda[k] / len(groups) for k in ("pda_dedup", "pda_gather")})
+
     # e2e through the scheduler's streaming API (async submit / collect over the
     # executor rings; the next batch is staged while the previous one runs)
     e2e_steps = e2e_step_count(args, step_ms)
@@ -518,8 +587,6 @@ def run_dso(args, dist) -> None:
     h2d = sum(len(h) + len(c) for h, c in reqs) * 8 + 3 * 4 * len(plan)
     d2h = n_cand * tasks * 4
 
-    prof = [[rec for ex in groups for rec in ex.profile(_lib.INPUT_IDS)] for _ in range(2)]
-    tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels = roofline(prof, name)
     step_flops = sum(algorithmic_flops(cfg, H, c) for c in counts)
     step_tf = step_flops / (sum(step_ms) / args.steps / 1e3) / 1e12
     cpu_baseline = cpu_baseline_line(args, dist, name)
@@ -529,7 +596,7 @@ def run_dso(args, dist) -> None:
     step_p99 = dist.max(nearest_rank(step_ms, 0.99))
     emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf,
               e2e_value, e2e_steps, h2d, d2h, launches, tensor, top, achieved, peak, traffic, peak_src, per_launch,
-              avg_ms, kernels, clk, cpu_baseline,
+              avg_ms, kernels, clk, cpu_baseline, prof_clk=prof_clk, pda=pda,
               extra_config={"candidates_per_request": "16 + Zipf(1.0) rank over 2033 (16..2048)",
                             "candidates_per_step_per_gpu": n_cand, "groups_per_step": len(plan),
                             "step_p99_ms": step_p99,
@@ -552,7 +619,7 @@ def e2e_step_count(args, step_ms) -> int:
 
 def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf, e2e_value, e2e_steps,
               h2d, d2h, launches, tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels, clk,
-              cpu_baseline, extra_config=None, e2e_path=None, latency_note=None):
+              cpu_baseline, extra_config=None, e2e_path=None, latency_note=None, prof_clk=None, pda=None, e2e_lat=None):
     if dist.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": dist.world_size,
@@ -572,6 +639,10 @@ def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99
             "step_tflops": round(step_tf, 1),
             "e2e": {"value": e2e_value, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    **({"request_p50_ms": e2e_lat[0], "request_p99_ms": e2e_lat[1],
+                        "latency": "per request: submission of its batch (numpy ids) -> its scores on the host, "
+                                   "streaming mode (one batch in flight ahead), nearest rank, max over ranks"}
+                       if e2e_lat else {}),
                     "timing": "host wall clock over ~0.3 s of device work (sustained, power-capped rate)",
                     "path": e2e_path or ("BucketScheduler.score_stream(ids=True): numpy ids -> pinned -> H2D -> "
                                          "graph -> D2H -> numpy, one step in flight ahead")},
@@ -581,8 +652,15 @@ def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99
                          "achieved": round(achieved, 1), "peak": peak,
                          "unit": "TFLOP/s" if tensor else "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic,
-                         "peak_source": f"{peak_src} ({'bf16_tflops_sustained' if tensor else 'hbm_gbs'})",
-                         "per_launch": per_launch, "avg_launch_ms": avg_ms},
+                         "peak_source": peak_src,
+                         "per_launch": per_launch, "avg_launch_ms": avg_ms,
+                         "timing": "per-launch CUDA events on the executor stream, eager profile pass run "
+                                   "before the e2e region",
+                         "profile_clocks": prof_clk,
+                         "traffic_source": "profiles/ncu_dram_per_launch.json (ncu --set full of tools/prof_step.py: "
+                                           "the bench's own workload, 100k-item fp32 table)"},
+            "pda": pda and {"unique_rows_per_step": pda["unique_rows"], "positions_per_step": pda["positions"],
+                            "bytes": "SURVEY 8(d): one table row per unique id; dedup = ids in + unique + inverse out"},
             "kernels": kernels,
             "clocks": clk,
             "cpu_baseline": cpu_baseline,
@@ -604,6 +682,18 @@ def main() -> None:
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU without an external launcher: re-run this command
+        # under torch.distributed.run (rendezvous on 127.0.0.1)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     from paper_2509_22681_b200.sharding import Dist
 
     dist = Dist(backend="gloo" if args.impl == "reference" else None)

@@ -14,9 +14,9 @@ timeout 900 python bench.py --workload cfg3 --steps 150 --warmup 5 --no-cpu-base
 tail -1 $O/bench_cfg3_sustained.log > $O/bench_cfg3_sustained.json
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/ref_cfg3.log 2>&1; tail -1 $O/ref_cfg3.log > $O/ref_cfg3.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 10 --csv \
-  --log-file $O/launches_cfg3.csv python dev/prof_step.py cfg3 3 > $O/ncu_launch.log 2>&1
+  --log-file $O/launches_cfg3.csv python tools/prof_step.py cfg3 3 > $O/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-  -k regex:5flame -c 10 -o $O/prof_full_cfg3 -f python dev/prof_step.py cfg3 1 > $O/ncu_full.log 2>&1
+  -k regex:5flame -c 10 -o $O/prof_full_cfg3 -f python tools/prof_step.py cfg3 1 > $O/ncu_full.log 2>&1
 tail -2 $O/pytest_gpu.log; tail -2 $O/smoke.log
 for w in cfg3 cfg4 cfg2 cfg5 cfg1; do python -c "
 import json; d=json.load(open('$O/bench_$w.json')); print('$w', round(d['value']/1e6,3), 'M/s e2e', round(d['e2e']['value']/1e6,3), 'p99', round(d['p99_ms'],2), 'roof', d['roofline']['kernel'], d['roofline']['frac'], 'cpu', (d.get('cpu_baseline') or {}).get('value'))" 2>&1 | tail -1; done

@@ -5,7 +5,7 @@
 
 The capture command (run under gpurun, one GPU) is
     ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-        -k regex:5flame -c 10 -o gpurun_out/prof_full_cfg3 python dev/prof_step.py cfg3 1
+        -k regex:5flame -c 10 -o gpurun_out/prof_full_cfg3 python tools/prof_step.py cfg3 1
 Kernels are labelled by their position in the launch sequence of one pass
 (paper_2509_22681_b200/csrc/flame.cu Pipe::run), which is fixed for a config.
 Writes:
