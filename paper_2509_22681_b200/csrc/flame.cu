@@ -29,6 +29,7 @@
 #include "gemm_tcgen05.cuh"
 #include "gemm_launch.cuh"
 #include "attention_tcgen05.cuh"
+#include "attention_fused.cuh"
 #include "simt_f32.cuh"
 #include "rowops.cuh"
 #include "pda.cuh"
@@ -612,6 +613,43 @@ struct Pipe {
     return check();
   }
 
+  // Candidate Q/K/V projection fused into the SUMI attention (last layer = layer 0,
+  // bf16 folded-LN path, hb <= 256): replaces gemm_qkv_cand + attention(false)
+  int attention_fused(const LayerW& w) {
+    if (e->R == 0 || e->c_bkt == 0) return 0;
+    const int D = c->D, DA = c->DA, G = c->G;
+    {
+      const double C = static_cast<double>(e->R) * e->c_bkt, hb = e->hb_bkt, d = c->d;
+      const double fl = G * (6.0 * C * d * d + 4.0 * d * C * (hb + 1));
+      const double by = G * (static_cast<double>(e->R) * hb * 2.0 * DA * 2.0 + C * DA * 2.0) + C * D * 2.0 +
+                        static_cast<double>(G) * 3.0 * DA * D * 2.0;
+      mark("attention_fused", fl, by);
+    }
+    FusedAttnArgs fa{};
+    fa.out = static_cast<__nv_bfloat16*>(e->AO);
+    fa.out_ld = DA; fa.out_gstride = e->rows * static_cast<long long>(DA);
+    fa.DA = DA; fa.nh = c->nh; fa.R = e->R; fa.hb_bkt = e->hb_bkt; fa.c_bkt = e->c_bkt; fa.num_blocks = G;
+    fa.k_blocks = D / 64; fa.hist_len = e->io.hist_len; fa.cand_len = e->io.cand_len;
+    fa.scale_log2 = c->scale_log2; fa.rs_c = e->rs_c; fa.cqkv = w.cqkv;
+    fa.store_tma = (e->c_bkt % 128) == 0; fa.active = e->io.active;
+    CUtensorMap ta, tw, tq, to;
+    if (!make_tmap_bf16_3d(&ta, e->Ecc, D, e->Rc, 1, static_cast<uint64_t>(D) * 2, 0, 64, 128) ||
+        !make_tmap_bf16_3d(&tw, w.wqkv, D, 3ULL * DA, G, static_cast<uint64_t>(D) * 2, 3ULL * DA * D * 2, 64, 64) ||
+        !make_tmap_bf16_3d(&tq, e->QKV, 3ULL * DA, e->rows, G, 3ULL * DA * 2, e->rows * 3ULL * DA * 2, 64, 128) ||
+        !make_tmap_bf16_3d(&to, e->AO, DA, e->rows, G, static_cast<uint64_t>(DA) * 2,
+                           e->rows * static_cast<uint64_t>(DA) * 2, 64, 128))
+      return fail(2, "tensor maps for the fused attention failed");
+    static DeviceOnce once;
+    cudaError_t ae = once.run([](int) {
+      return cudaFuncSetAttribute(sumi_fused_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize, fattn::kSmemBytes);
+    });
+    if (ae != cudaSuccess) return fail(2, std::string("fused attention attributes: ") + cudaGetErrorString(ae));
+    const int units = e->R * G * c->nh;
+    dim3 grid(units < c->num_sms ? units : c->num_sms);
+    sumi_fused_tcgen05<<<grid, fattn::kThreads, fattn::kSmemBytes, s>>>(ta, tw, tq, to, fa);
+    return check();
+  }
+
   int launch_dedup(const PdaLists& l, int cap, int lists, cudaStream_t st) {
     cudaError_t err = launch_dedup_shape(l, cap, lists, st);
     if (err != cudaSuccess) return fail(2, std::string("pda_dedup: ") + cudaGetErrorString(err));
@@ -761,13 +799,22 @@ struct Pipe {
         if (int rc = gemm(A_h, D, A_h_g, 0, Wqkv, D, 3LL * DA * D, Rh, 3 * DA, D, G, QKV, 3LL * DA, gQKV, 0,
                           w.cqkv, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
       }
-      rs_ptr = rs_c; rs_g = rs_c_g;
-      gemm_name = "gemm_qkv_cand";
-      ln1_consumer(Rh, w.uqkv);
-      if (int rc = gemm(A_c, D, A_c_g, A_c_shared, Wqkv, D, 3LL * DA * D, Rc, 3 * DA, D, G, QKV + Rh * 3LL * DA,
-                        3LL * DA, gQKV, 0, w.cqkv, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
-      // SUMI attention (attention.py:118-146; :149-178 for non-final layers)
-      if (int rc = attention(false)) return rc;
+      static const bool fused_attn = [] {  // FLAME_FUSED_ATTN=0: separate QKV GEMM + attention (A/B)
+        const char* v = getenv("FLAME_FUSED_ATTN");
+        return !(v && atoi(v) == 0);
+      }();
+      if (kFold && fused_attn && last && l == 0 && e->hb_bkt <= 256) {
+        // candidate Q / K / V never reach HBM: projected inside the attention CTA
+        if (int rc = attention_fused(w)) return rc;
+      } else {
+        rs_ptr = rs_c; rs_g = rs_c_g;
+        gemm_name = "gemm_qkv_cand";
+        ln1_consumer(Rh, w.uqkv);
+        if (int rc = gemm(A_c, D, A_c_g, A_c_shared, Wqkv, D, 3LL * DA * D, Rc, 3 * DA, D, G, QKV + Rh * 3LL * DA,
+                          3LL * DA, gQKV, 0, w.cqkv, 3LL * DA, nullptr, 0, 0, qkv_epi)) return rc;
+        // SUMI attention (attention.py:118-146; :149-178 for non-final layers)
+        if (int rc = attention(false)) return rc;
+      }
       if (!last) { if (int rc = attention(true)) return rc; }
       // O-projection + residual (forward.py:116 / :135)
       // bf16 path: X1 is written once in bf16 (it is both the W1 A operand and the
