@@ -202,15 +202,56 @@ def _oracle_worker(args):
     return time.perf_counter() - t_all, lat
 
 
+# the unmodified reference, pip-installed offline into baseline/_ref;
+# when present the CPU arm runs IT, else the oracle port pinned to it
+REF_PKG = ROOT / "baseline" / "_ref"
+REF_AVAILABLE = (REF_PKG / "flameserve" / "service.py").exists()
+CPU_KIND = "reference" if REF_AVAILABLE else "port"
+CPU_WHAT = ("unmodified reference (baseline/_ref) Service.handle_request: sync feature cache over the "
+            "simulated store (0 ms latency), implicit-shape runner -> numpy fp64 model_forward"
+            if REF_AVAILABLE else
+            "numpy fp64 oracle port of reference resolve_embeddings + model_forward")
+
+
+def _reference_worker(args):
+    """The reference's own request path (service.py:127-171) on one host process."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    name, reqs = args
+    sys.path.insert(0, str(REF_PKG))
+    from flameserve.cache import CacheConfig, CacheMode
+    from flameserve.config import OrchestratorConfig, ServiceConfig
+    from flameserve.model import ModelConfig
+    from flameserve.service import ScoreRequest, Service
+    from flameserve.store import RemoteStoreConfig
+
+    c = model_config(name)
+    cfg = ServiceConfig(
+        model=ModelConfig(c.hidden_dim, c.head_dim, c.num_blocks, c.layers_per_block, c.ffn_dim, c.num_tasks,
+                          c.max_history_len, c.max_candidates, seed=c.seed),
+        cache=CacheConfig(mode=CacheMode.SYNC), remote_store=RemoteStoreConfig(0.0, 0.0, seed=STORE_SEED),
+        orchestrator=OrchestratorConfig(routing="implicit"))
+    svc = Service(cfg)
+    lat = []
+    t_all = time.perf_counter()
+    for k, (hid, cid) in enumerate(reqs):
+        t0 = time.perf_counter()
+        svc.handle_request(ScoreRequest(user_id=k, history_item_ids=hid, candidate_item_ids=cid))
+        lat.append(time.perf_counter() - t0)
+    busy = time.perf_counter() - t_all
+    svc.close()
+    return busy, lat
+
+
 def cpu_reference_sample(name: str, n_requests: int, procs: int, seed: int) -> dict:
-    """Time the oracle port on ``procs`` host processes (1 BLAS thread each)."""
+    """Time the reference CPU path (or, without baseline/_ref, the oracle port) on
+    ``procs`` host processes (1 BLAS thread each)."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     reqs = make_requests(n_requests, WORKLOADS[name][6], WORKLOADS[name][7], seed, name in ZIPF_C)
     chunks = [(name, reqs[i::procs]) for i in range(procs) if reqs[i::procs]]
     ctx = mp.get_context("spawn")
     t0 = time.perf_counter()
     with ctx.Pool(len(chunks)) as pool:
-        res = pool.map(_oracle_worker, chunks)
+        res = pool.map(_reference_worker if REF_AVAILABLE else _oracle_worker, chunks)
     wall = time.perf_counter() - t0
     lat = sorted(x for _, l in res for x in l)
     return {"wall_s": wall, "busy_s": max(r[0] for r in res), "requests": n_requests,
@@ -255,10 +296,9 @@ def run_reference(args, dist) -> None:
         "config": {"workload": name, "desc": WORKLOADS[name][9], "requests_per_step": per * procs,
                    "candidates_per_request": C, "history_len": WORKLOADS[name][6]},
         "p99_ms": 1000 * nearest_rank(lats, 0.99),
-        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": procs, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": procs, "kind": CPU_KIND,
                          "sample": f"{per * procs} requests per step ({procs} processes x 1 BLAS thread) "
-                                   f"on {cpu}; numpy fp64 oracle port of reference "
-                                   "resolve_embeddings + model_forward"},
+                                   f"on {cpu}; {CPU_WHAT}"},
         "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -315,6 +355,7 @@ def roofline(prof_runs: list, name: str, prof_clk: dict | None = None, byte_over
     follows the profile pass's own clock record (``choose_peak``)."""
     n_runs = len(prof_runs)
     agg: dict = {}
+    times: dict = {}
     for run in prof_runs:
         for rec in run:
             a = agg.setdefault(rec["name"], {"ms": 0.0, "n": 0, "flops": 0.0, "bytes": 0.0})
@@ -322,6 +363,11 @@ def roofline(prof_runs: list, name: str, prof_clk: dict | None = None, byte_over
             a["n"] += 1
             a["flops"] += rec["flops"]
             a["bytes"] += (byte_override or {}).get(rec["name"], rec["bytes"])
+            times.setdefault(rec["name"], []).append(rec["ms"])
+    # per-launch time = the median over the eager passes (one launch per role and
+    # pass): robust to a single pass disturbed by host scheduling
+    for k, a in agg.items():
+        a["ms"] = statistics.median(times[k]) * a["n"]
     step_prof_ms = sum(a["ms"] for a in agg.values()) / n_runs
     top = max(agg, key=lambda k: agg[k]["ms"])
     t = agg[top]
@@ -352,6 +398,7 @@ def roofline(prof_runs: list, name: str, prof_clk: dict | None = None, byte_over
 def profile_pass(ex, mode, runs: int, dev_index: int):
     """Per-launch CUDA-event profile of ``runs`` eager passes with its own NVML
     clock record (the roofline's peak is chosen from these clocks)."""
+    ex.profile(mode)  # one untimed eager pass: host-side first-use work stays out of the record
     clocks = ClockSampler(dev_index, period_s=0.002)
     clocks.start()
     clocks.begin()
@@ -360,17 +407,17 @@ def profile_pass(ex, mode, runs: int, dev_index: int):
 
 
 def cpu_baseline_line(args, dist, name: str):
-    """The oracle port on this host's cores (rank 0, N = 1 only), bounded sample."""
+    """The reference CPU path (or the oracle port) on this host's cores (rank 0,
+    N = 1 only), bounded sample."""
     if dist.world_size != 1 or args.no_cpu_baseline:
         return None
     cores = len(os.sched_getaffinity(0))
     procs = max(1, min(cores, 32, int(os.environ.get("FLAME_BENCH_CPU_PROCS", "32"))))
     n_req = procs * 2 * REF_REQS_PER_PROC.get(name, 1)
     r = cpu_reference_sample(name, n_req, procs, WORKLOAD_SEED + 99)
-    return {"value": r["cands"] / r["busy_s"], "unit": "candidates/s", "cores": r["procs"], "kind": "port",
+    return {"value": r["cands"] / r["busy_s"], "unit": "candidates/s", "cores": r["procs"], "kind": CPU_KIND,
             "sample": f"{n_req} requests of {name} on {r['procs']} processes x 1 BLAS thread "
-                      f"({_cpu_name()}), numpy fp64 oracle port of reference "
-                      f"resolve_embeddings + model_forward; compute {r['busy_s']:.1f}s; "
+                      f"({_cpu_name()}), {CPU_WHAT}; compute {r['busy_s']:.1f}s; "
                       f"p99 {1000 * nearest_rank(r['lat'], 0.99):.0f} ms"}
 
 

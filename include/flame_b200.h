@@ -158,6 +158,43 @@ void* flame_exec_workspace(FlameExec* ex, const char* name);
 /* Synchronous device-to-host copy (test / debugging helper). */
 int flame_copy_to_host(void* dst_host, const void* src_device, long long bytes);
 
+/* ---------------------------------------------------------------- operators
+ * The reference's operator-level API (model/__init__.py:4-31) over host fp64
+ * arrays, computed on the device (synchronous; results written to `out`).
+ *
+ * flame_op_attention_sumi replaces model/attention.py:118-146
+ *   attention_sumi_candidates (candidates_only = 1: q is (num_heads, C, head_dim)
+ *   with C = seq_len - hist_len, out likewise) and :149-178 attention_sumi
+ *   (candidates_only = 0: q and out are (num_heads, seq_len, head_dim)); k / v are
+ *   (num_heads, seq_len, head_dim).  Runs the forward pass's SUMI attention
+ *   kernels (bf16 tcgen05 or fp32 verification); head_dim <= 64.
+ * flame_op_attention_masked replaces attention.py:55-67 attention_naive /
+ *   :70-115 attention_tiled: one head, (seq_len, head_dim) q / k / v and an
+ *   arbitrary seq_len x seq_len permission matrix (1 = allowed), in fp64.
+ * flame_op_rows replaces forward.py:33-47 gelu / sigmoid / layer_norm and
+ *   attention.py:28-36 masked_softmax_rows, fp64, rows x width row-major
+ *   (layer_norm: scale / shift of length width).
+ * flame_op_gated_fusion replaces forward.py:143-156 gated_fusion:
+ *   block_outputs [num_blocks][rows][width], gate_w / gate_b [num_blocks][width].
+ * flame_op_block_states replaces forward.py:75-140 block_forward for every block
+ *   of the context at once: out [num_blocks][cand_count][hidden_dim] = each
+ *   block's final candidate rows over its contiguous history split.
+ * flame_op_expert_heads replaces forward.py:159-166 expert_heads:
+ *   fused [rows][hidden_dim] -> out [rows][num_tasks]. */
+enum FlameRowOp { FLAME_OP_GELU = 0, FLAME_OP_SIGMOID = 1, FLAME_OP_LAYER_NORM = 2, FLAME_OP_SOFTMAX = 3 };
+int flame_op_attention_sumi(int precision, int device, int num_heads, int seq_len, int head_dim, int hist_len,
+                            int candidates_only, double temperature, const double* q, const double* k,
+                            const double* v, double* out);
+int flame_op_attention_masked(int device, int seq_len, int head_dim, double temperature, const double* q,
+                              const double* k, const double* v, const unsigned char* allowed, double* out);
+int flame_op_rows(int op, int device, long long rows, int width, const double* x, const double* scale,
+                  const double* shift, double* out);
+int flame_op_gated_fusion(int device, int num_blocks, long long rows, int width, const double* block_outputs,
+                          const double* gate_w, const double* gate_b, double* out);
+int flame_op_block_states(FlameCtx* ctx, const double* history, long long hist_len, const double* candidates,
+                          long long cand_count, double* out);
+int flame_op_expert_heads(FlameCtx* ctx, const double* fused, long long rows, double* out);
+
 const char* flame_last_error(void);
 int flame_device_sm_count(int device);
 

@@ -27,7 +27,10 @@ EXPORTED = (
     "flame_exec_capture", "flame_exec_replay", "flame_exec_launch_count", "flame_exec_workspace",
     "flame_exec_profile",
     "flame_last_error", "flame_device_sm_count", "flame_copy_to_host",
+    "flame_op_attention_sumi", "flame_op_attention_masked", "flame_op_rows", "flame_op_gated_fusion",
+    "flame_op_block_states", "flame_op_expert_heads",
 )
+OP_GELU, OP_SIGMOID, OP_LAYER_NORM, OP_SOFTMAX = 0, 1, 2, 3
 
 
 class FlameModelDesc(ctypes.Structure):
@@ -88,6 +91,12 @@ def load() -> ctypes.CDLL:
             "flame_last_error": (ctypes.c_char_p, []),
             "flame_device_sm_count": (I, [I]),
             "flame_copy_to_host": (I, [P, P, LL]),
+            "flame_op_attention_sumi": (I, [I, I, I, I, I, I, I, ctypes.c_double, P, P, P, P]),
+            "flame_op_attention_masked": (I, [I, I, I, ctypes.c_double, P, P, P, P, P]),
+            "flame_op_rows": (I, [I, I, LL, I, P, P, P, P]),
+            "flame_op_gated_fusion": (I, [I, I, LL, I, P, P, P, P]),
+            "flame_op_block_states": (I, [P, P, LL, P, LL, P]),
+            "flame_op_expert_heads": (I, [P, P, LL, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

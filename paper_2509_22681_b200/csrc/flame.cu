@@ -727,6 +727,11 @@ struct Pipe {
     return 0;
   }
 
+  // operator-level block_forward (flame_op_block_states): stop after the layer stacks
+  // and leave every block's final hidden rows in final_x ([G][rows][D] fp32)
+  bool block_states = false;
+  float* final_x = nullptr;
+
   int run(int mode) {
     if (int rc = assemble(mode)) return rc;
     if (mode == FLAME_INPUT_GATHER_ONLY) return 0;
@@ -853,7 +858,7 @@ struct Pipe {
                           Hf + r0 * F, F, gF, 0, w.b1, F, nullptr, 0, 0, EPI_BIAS | EPI_GELU)) return rc;
       }
       gemm_name = "gemm_ffn_w2";
-      if (kFold && last && fuse_gate) {
+      if (kFold && last && fuse_gate && !block_states) {
         // last layer: the W2 epilogue also performs the gated fusion over blocks
         // (forward.py:143-156) and writes only the fp32 sum, the tf32 expert operand
         resid_b = reinterpret_cast<const __nv_bfloat16*>(Y) + r0 * D;
@@ -881,6 +886,10 @@ struct Pipe {
       }
       Xcur = Xnext;
     }
+    if (block_states) {
+      final_x = Xcur;
+      return 0;
+    }
     // gated fusion over blocks (forward.py:143-156)
     if (!gated_done) {
       const long long n = Rc * (D / 4);
@@ -889,7 +898,14 @@ struct Pipe {
           Xcur + Rh * D, D, gD, G, c->gate_w, c->gate_b, static_cast<float*>(e->Fz), D, static_cast<int>(Rc), D);
       if (int rc = check()) return rc;
     }
-    // expert heads (forward.py:159-166)
+    return experts();
+  }
+
+  // expert heads (forward.py:159-166) over the fused rows in e->Fz
+  int experts() {
+    constexpr bool kFold = std::is_same<Act, __nv_bfloat16>::value;
+    const int D = c->D, F = c->F;
+    const long long Rc = e->Rc;
     gemm_name = "gemm_expert_w1";
     if (kFold && c->tasks <= 4) {
       // fp32 fused rows x fp32 W_e1, multiplied as tf32 (kind::tf32); the epilogue applies
@@ -1365,6 +1381,8 @@ void* flame_exec_workspace(FlameExec* e, const char* name) {
 }
 
 }  // extern "C"
+
+#include "ops_abi.cuh"
 
 // Debug-only (not part of the public header): route the attention kernel's CTA-0
 // event trace into a caller-owned device buffer of 4 x 4096 uint64 (NULL = off).

@@ -96,6 +96,15 @@ def get_engine(params: ModelParams, config: ModelConfig, precision: str = DEFAUL
         return eng
 
 
+def find_engine(params: ModelParams, precision: str = DEFAULT_PRECISION, device=None):
+    """An engine already built for ``params`` (any config), or None."""
+    with _engines_lock:
+        for (_, prec, dev, fp), eng in (_engines.get(id(params)) or {}).items():
+            if prec == precision and dev == device and fp == _fingerprint(params):
+                return eng
+    return None
+
+
 def model_forward(
     history: np.ndarray,
     candidates: np.ndarray,

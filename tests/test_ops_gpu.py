@@ -1,0 +1,118 @@
+"""Device parity of the operator-level API (§8(b)) against the reference's own
+operator outputs (tests/golden/ops.npz, oracle/gen_golden_ops.py).
+
+Tolerances: the fp64 device helpers (gelu, sigmoid, layer_norm, masked softmax,
+masked attention) 1e-12; operators on the forward pass's kernels: fp32
+verification mode 1e-5 (attention, fusion, experts) / 1e-4 (block states);
+bf16 mode: attention outputs 2e-2 (q/k/v rounded to bf16, |v| <= 1), block
+states 5e-2 (hidden states of magnitude ~3 through bf16 GEMMs), expert scores
+2e-2 (the north-star score tolerance).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2509_22681_b200 as fb
+from conftest import load_golden
+from oracle.gen_golden_ops import BLOCK_CASES, SUMI_CASES, block_inputs, sumi_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def blob():
+    return load_golden("ops.npz")
+
+
+def _close(a, b, tol, what):
+    err = float(np.abs(np.asarray(a) - np.asarray(b)).max()) if np.asarray(b).size else 0.0
+    assert err <= tol, f"{what}: max abs {err:.3e} > {tol}"
+
+
+def test_row_helpers(gpu, blob):
+    x, s = blob["rows_x"], blob["rows_s"]
+    _close(fb.gelu(x), blob["gelu"], 1e-12, "gelu")
+    _close(fb.sigmoid(x), blob["sigmoid"], 1e-12, "sigmoid")
+    _close(fb.layer_norm(x, blob["ln_scale"], blob["ln_shift"]), blob["layer_norm"], 1e-12, "layer_norm")
+    _close(fb.masked_softmax_rows(s), blob["softmax"], 1e-12, "softmax")
+    assert fb.gelu(np.zeros((0, 4))).shape == (0, 4)
+
+
+def test_masked_attention_any_mask(gpu, blob):
+    q, k, v = blob["mq"], blob["mk"], blob["mv"]
+    rand = fb.SumiMask(0, q.shape[0], blob["mask_rand"])
+    _close(fb.attention_naive(q, k, v, rand, 0.9), blob["naive_rand"], 1e-12, "naive / random mask")
+    _close(fb.attention_tiled(q, k, v, rand, 0.9, 16), blob["tiled_rand"], 1e-12, "tiled / random mask")
+    _close(fb.attention_naive(q, k, v, fb.build_sumi_mask(50, 20), 1.1), blob["naive_sumi"], 1e-12, "naive / SUMI")
+    assert fb.attention_naive(q[:0], k[:0], v[:0], fb.build_sumi_mask(0, 0), 1.0).shape == (0, 24)
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-5), ("bf16", 2e-2)])
+@pytest.mark.parametrize("i", range(len(SUMI_CASES)))
+def test_sumi_attention_operators(gpu, blob, i, prec, tol):
+    nh, dh, h, c, tau = SUMI_CASES[i]
+    q, k, v = sumi_inputs(i)
+    cand = fb.attention_sumi_candidates(q[:, h:], k, v, h, tau, precision=prec)
+    assert cand.shape == (nh, c, dh)
+    _close(cand, blob[f"sumi{i}_cand"], tol, f"attention_sumi_candidates case {i} {prec}")
+    full = fb.attention_sumi(q, k, v, h, tau, precision=prec)
+    assert full.shape == q.shape
+    _close(full, blob[f"sumi{i}_all"], tol, f"attention_sumi case {i} {prec}")
+    # the candidate rows of the full operator are the candidates-only operator, bit for bit
+    np.testing.assert_array_equal(full[:, h:], cand)
+
+
+def test_sumi_attention_rejects_wide_heads(gpu):
+    q = np.zeros((1, 4, 128))
+    with pytest.raises(ValueError, match="head_dim"):
+        fb.attention_sumi(q, q, q, 2, 1.0)
+
+
+def _block_case(i):
+    d, dh, nb, layers, f, tasks, hl, cc = BLOCK_CASES[i]
+    cfg = fb.ModelConfig(d, dh, nb, layers, f, tasks, max(hl, nb), max(cc, 1), seed=40 + i)
+    hist, cand = block_inputs(i)
+    return cfg, fb.init_params(cfg), hist, cand
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("bf16", 5e-2)])
+@pytest.mark.parametrize("i", range(len(BLOCK_CASES)))
+def test_block_forward(gpu, blob, i, prec, tol):
+    cfg, params, hist, cand = _block_case(i)
+    subs = fb.split_sequence(hist, cfg.num_blocks)
+    for b, (sub, blk) in enumerate(zip(subs, params.blocks)):
+        out = fb.block_forward(sub, cand, blk, cfg, precision=prec)
+        assert out.shape == cand.shape
+        _close(out, blob[f"blk{i}_outs"][b], tol, f"block_forward case {i} block {b} {prec}")
+
+
+@pytest.mark.parametrize("i", range(len(BLOCK_CASES)))
+def test_gated_fusion_and_expert_heads(gpu, blob, i):
+    cfg, params, _, _ = _block_case(i)
+    outs = list(blob[f"blk{i}_outs"])
+    fused = fb.gated_fusion(outs, params)
+    ref = blob[f"blk{i}_fused"]
+    _close(fused, ref, 1e-5 * max(1.0, float(np.abs(ref).max())), f"gated_fusion case {i}")
+    for prec, tol in (("fp32", 1e-5), ("bf16", 2e-2)):
+        scores = fb.expert_heads(blob[f"blk{i}_fused"], params, precision=prec)
+        assert scores.shape == blob[f"blk{i}_scores"].shape
+        _close(scores, blob[f"blk{i}_scores"], tol, f"expert_heads case {i} {prec}")
+
+
+def test_operators_compose_to_model_forward(gpu):
+    # block_forward -> gated_fusion -> expert_heads reproduces model_forward
+    # (reference forward.py:195-204) within the fp32 tolerance
+    cfg, params, hist, cand = _block_case(0)
+    outs = [fb.block_forward(s, cand, b, cfg, precision="fp32")
+            for s, b in zip(fb.split_sequence(hist, cfg.num_blocks), params.blocks)]
+    scores = fb.expert_heads(fb.gated_fusion(outs, params), params, precision="fp32")
+    ref = fb.model_forward(hist, cand, params, cfg, precision="fp32")
+    _close(scores, ref, 1e-5, "composed operators vs model_forward")
+
+
+def test_model_forward_sequential_matches_golden(gpu):
+    from conftest import golden_forward
+
+    cfg, params, hist, cand, blob = golden_forward("ref_instance")
+    out = fb.model_forward_sequential(hist, cand, params, cfg, precision="fp32")
+    _close(out, blob["sequential"], 1e-4, "model_forward_sequential")

@@ -28,6 +28,9 @@ from pathlib import Path
 # (the gated fusion runs inside the FFN W2 epilogue of the last layer)
 ROLES_L1 = ["pda_dedup", "pda_gather", "gemm_kv_hist", "gemm_qkv_cand", "attention_sumi",
             "gemm_oproj_cand", "gemm_ffn_w1", "gemm_ffn_w2", "gemm_expert_w1", "expert_combine"]
+# the same with the candidate Q/K/V projection fused into the attention (hb <= 256)
+ROLES_L1_FUSED = ["pda_dedup", "pda_gather", "gemm_kv_hist", "attention_fused",
+                  "gemm_oproj_cand", "gemm_ffn_w1", "gemm_ffn_w2", "gemm_expert_w1", "expert_combine"]
 
 METRICS = {
     "duration_ms": "gpu__time_duration.sum",
@@ -41,7 +44,7 @@ METRICS = {
     "l2_hit_pct": "lts__t_sector_hit_rate.pct",
 }
 
-OURS = re.compile(r"pda_|gemm_bf16|gemm_f32|sumi_attention|gated_fusion|expert_|layer_norm_rows|scatter_emb")
+OURS = re.compile(r"pda_|gemm_bf16|gemm_f32|sumi_attention|sumi_fused|gated_fusion|expert_|layer_norm_rows|scatter_emb")
 
 UNIT_SCALE = {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "s": 1e3,
               "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
@@ -76,7 +79,7 @@ def main() -> None:
     args = ap.parse_args()
     args.out.mkdir(parents=True, exist_ok=True)
     ks = [k for k in ncu_raw(args.full) if OURS.search(k["kernel"])]
-    roles = ROLES_L1 if len(ks) == len(ROLES_L1) else [f"k{i}" for i in range(len(ks))]
+    roles = next((r for r in (ROLES_L1, ROLES_L1_FUSED) if len(r) == len(ks)), [f"k{i}" for i in range(len(ks))])
     total = sum(k["duration_ms"] for k in ks)
     with open(args.out / f"ncu_kernels_{args.workload}.csv", "w", newline="") as fh:
         w = csv.writer(fh)
