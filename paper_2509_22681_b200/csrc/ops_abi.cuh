@@ -143,7 +143,7 @@ inline double from_act(__nv_bfloat16 v) { return static_cast<double>(__bfloat162
 
 // SUMI attention over one request through the forward pass's kernels:
 // Pipe::attention on a one-request, one-block executor whose QKV rows hold the
-// caller's q / k / v (head h in lanes [h*64, h*64+dh) of each third).
+// caller's q / k / v (head h in lanes [h*HS, h*HS+dh) of each third, HS = 64 or 128).
 template <typename Act>
 int op_attention(int device, int nh, int T, int dh, int h, int cand_only, double temperature, const double* q,
                  const double* k, const double* v, double* out) {
@@ -152,7 +152,8 @@ int op_attention(int device, int nh, int T, int dh, int h, int cand_only, double
   c.precision = std::is_same<Act, __nv_bfloat16>::value ? FLAME_BF16 : FLAME_FP32;
   c.device = device;
   cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device);
-  c.nh = nh; c.dh = dh; c.G = 1; c.DA = nh * 64; c.d = nh * dh; c.D = pad_to(c.d, 64);
+  c.HS = dh <= 64 ? 64 : 128;
+  c.nh = nh; c.dh = dh; c.G = 1; c.DA = nh * c.HS; c.d = nh * dh; c.D = pad_to(c.d, 64);
   c.act_bytes = sizeof(Act);
   OpBufs b;
   const double sc = 1.0 / (temperature * std::sqrt(static_cast<double>(dh)));
@@ -174,7 +175,7 @@ int op_attention(int device, int nh, int T, int dh, int h, int cand_only, double
   std::vector<Act> hq(rows * 3 * DA, to_act<Act>(0.0));
   for (int hd = 0; hd < nh; ++hd)
     for (int t = 0; t < T; ++t) {
-      Act* row = hq.data() + static_cast<size_t>(t) * 3 * DA + static_cast<size_t>(hd) * 64;
+      Act* row = hq.data() + static_cast<size_t>(t) * 3 * DA + static_cast<size_t>(hd) * c.HS;
       const bool has_q = !cand_only || t >= h;
       const long long qt = cand_only ? t - h : t;
       const long long qrows = cand_only ? C : T;
@@ -210,7 +211,7 @@ int op_attention(int device, int nh, int T, int dh, int h, int cand_only, double
     for (int t = t0; t < T; ++t)
       for (int l = 0; l < dh; ++l)
         out[(static_cast<long long>(hd) * orows + (t - t0)) * dh + l] =
-            from_act(ho[static_cast<size_t>(t) * DA + static_cast<size_t>(hd) * 64 + l]);
+            from_act(ho[static_cast<size_t>(t) * DA + static_cast<size_t>(hd) * c.HS + l]);
   return 0;
 }
 
@@ -306,7 +307,7 @@ int flame_op_attention_sumi(int precision, int device, int num_heads, int seq_le
                             const double* v, double* out) {
   if (precision != FLAME_BF16 && precision != FLAME_FP32) return fail(1, "bad precision");
   if (num_heads < 1 || seq_len < 0 || head_dim < 1) return fail(1, "bad attention shape");
-  if (head_dim > 64) return fail(1, "head_dim above 64 is not supported by the SUMI attention kernels");
+  if (head_dim > 128) return fail(1, "head_dim above 128 is not supported by the SUMI attention kernels");
   if (hist_len < 0 || hist_len > seq_len)
     return fail(1, "hist_len " + std::to_string(hist_len) + " out of range for sequence length " +
                        std::to_string(seq_len));

@@ -126,30 +126,31 @@ __global__ void expert_out_rows(const TIn* __restrict__ hidden, long long h_ld,
                                 int F, int tasks, int c_bkt, const int* __restrict__ cand_len,
                                 const int* __restrict__ out_offset, float* __restrict__ out,
                                 int rows) {
-  constexpr int kMaxTasks = 8;
+  constexpr int kGroup = 8;  // tasks per pass over the hidden row
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   if (warp >= rows) return;
   const int r = warp / c_bkt, c = warp % c_bkt;
   if (c >= cand_len[r]) return;
-  float acc[kMaxTasks];
-#pragma unroll
-  for (int t = 0; t < kMaxTasks; ++t) acc[t] = 0.f;
   const TIn* hrow = hidden + static_cast<long long>(warp) * h_ld;
-  for (int k = lane; k < F; k += 32) {
-    const float hv = static_cast<float>(hrow[k]);
+  float* dst = out + static_cast<long long>(out_offset[r] + c) * tasks;
+  for (int t0 = 0; t0 < tasks; t0 += kGroup) {
+    float acc[kGroup];
 #pragma unroll
-    for (int t = 0; t < kMaxTasks; ++t)
-      if (t < tasks) acc[t] = fmaf(hv, w2[k * tasks + t], acc[t]);
-  }
+    for (int t = 0; t < kGroup; ++t) acc[t] = 0.f;
+    for (int k = lane; k < F; k += 32) {
+      const float hv = static_cast<float>(hrow[k]);
 #pragma unroll
-  for (int t = 0; t < kMaxTasks; ++t) {
+      for (int t = 0; t < kGroup; ++t)
+        if (t0 + t < tasks) acc[t] = fmaf(hv, w2[k * tasks + t0 + t], acc[t]);
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
-  }
-  if (lane == 0) {
-    float* dst = out + static_cast<long long>(out_offset[r] + c) * tasks;
-    for (int t = 0; t < tasks; ++t) dst[t] = sigmoid_f(acc[t] + b2[t]);
+    for (int t = 0; t < kGroup; ++t) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+    }
+    if (lane == 0)
+      for (int t = 0; t < kGroup && t0 + t < tasks; ++t) dst[t0 + t] = sigmoid_f(acc[t] + b2[t0 + t]);
   }
 }
 

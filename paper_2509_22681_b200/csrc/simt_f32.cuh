@@ -63,9 +63,10 @@ __global__ void __launch_bounds__(256) gemm_f32_simt(const float* __restrict__ A
   }
 }
 
-struct AttnArgsF32 {
-  const float* qkv;  // [G][rows][3*DA]
-  float* out;        // [G][rows][out_ld]
+template <typename T>
+struct AttnArgsSimt {
+  const T* qkv;  // [G][rows][3*DA]
+  T* out;        // [G][rows][out_ld]
   long long qkv_gstride, out_ld, out_gstride;
   int DA, R, hb_bkt, c_bkt, num_blocks;
   const int* hist_len;
@@ -73,12 +74,23 @@ struct AttnArgsF32 {
   const float* scale;  // [G] 1 / (tau_g * sqrt(head_dim))  (natural-exp domain)
 };
 
-// One thread = one query row; 64-key chunks of K/V staged in shared memory.
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f32(float v);
+template <>
+__device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// One thread = one query row; KC-key chunks of K/V staged in shared memory (fp32).
 // Same SUMI state update as the tcgen05 kernel: candidates start from the self
 // term (m = s_self, l = 1, o = v_self); history rows start empty and are causal.
-template <bool kHist>
-__global__ void __launch_bounds__(128) sumi_attention_f32(AttnArgsF32 a) {
-  constexpr int DH = 64, KC = 64;
+// T = float: the fp32 verification mode; T = bf16 with DH = 128: the head slots
+// wider than the tcgen05 kernel's 64 lanes (64 < head_dim <= 128), fp32 math.
+template <typename T, int DH, bool kHist>
+__global__ void __launch_bounds__(128) sumi_attention_simt(AttnArgsSimt<T> a) {
+  constexpr int KC = DH > 64 ? 32 : 64;
   __shared__ float sK[KC][DH + 1];
   __shared__ float sV[KC][DH + 1];
   const int h = blockIdx.y;
@@ -92,26 +104,26 @@ __global__ void __launch_bounds__(128) sumi_attention_f32(AttnArgsF32 a) {
   const long long grow = kHist ? static_cast<long long>(r) * a.hb_bkt + qi
                                : static_cast<long long>(a.R) * a.hb_bkt + static_cast<long long>(r) * a.c_bkt + qi;
   const long long ld = 3LL * a.DA;
-  const float* G0 = a.qkv + g * a.qkv_gstride;
+  const T* G0 = a.qkv + g * a.qkv_gstride;
   const float sc = a.scale[g];
   float q[DH], o[DH];
   float m, l;
   if (qi < bkt) {
-    const float* qrow = G0 + grow * ld + h * DH;
+    const T* qrow = G0 + grow * ld + h * DH;
 #pragma unroll
-    for (int e = 0; e < DH; ++e) q[e] = qrow[e];
+    for (int e = 0; e < DH; ++e) q[e] = to_f32(qrow[e]);
   } else {
 #pragma unroll
     for (int e = 0; e < DH; ++e) q[e] = 0.f;
   }
   if (!kHist && qi < bkt) {
-    const float* krow = G0 + grow * ld + a.DA + h * DH;
-    const float* vrow = G0 + grow * ld + 2 * a.DA + h * DH;
+    const T* krow = G0 + grow * ld + a.DA + h * DH;
+    const T* vrow = G0 + grow * ld + 2 * a.DA + h * DH;
     float dot = 0.f;
 #pragma unroll
-    for (int e = 0; e < DH; ++e) dot = fmaf(q[e], krow[e], dot);
+    for (int e = 0; e < DH; ++e) dot = fmaf(q[e], to_f32(krow[e]), dot);
 #pragma unroll
-    for (int e = 0; e < DH; ++e) o[e] = vrow[e];
+    for (int e = 0; e < DH; ++e) o[e] = to_f32(vrow[e]);
     m = dot * sc;
     l = 1.f;
   } else {
@@ -128,9 +140,9 @@ __global__ void __launch_bounds__(128) sumi_attention_f32(AttnArgsF32 a) {
     for (int e = threadIdx.x; e < KC * DH; e += 128) {
       const int kk = e / DH, dd = e % DH;
       const bool ok = k0 + kk < n_keys;
-      const float* rowp = G0 + (hist0 + k0 + kk) * ld;
-      sK[kk][dd] = ok ? rowp[a.DA + h * DH + dd] : 0.f;
-      sV[kk][dd] = ok ? rowp[2 * a.DA + h * DH + dd] : 0.f;
+      const T* rowp = G0 + (hist0 + k0 + kk) * ld;
+      sK[kk][dd] = ok ? to_f32(rowp[a.DA + h * DH + dd]) : 0.f;
+      sV[kk][dd] = ok ? to_f32(rowp[2 * a.DA + h * DH + dd]) : 0.f;
     }
     __syncthreads();
     int lim = min(KC, n_keys - k0);
@@ -150,10 +162,10 @@ __global__ void __launch_bounds__(128) sumi_attention_f32(AttnArgsF32 a) {
     }
   }
   if (row_ok) {
-    float* dst = a.out + g * a.out_gstride + grow * a.out_ld + h * DH;
+    T* dst = a.out + g * a.out_gstride + grow * a.out_ld + h * DH;
     const float inv = 1.f / l;
 #pragma unroll
-    for (int e = 0; e < DH; ++e) dst[e] = o[e] * inv;
+    for (int e = 0; e < DH; ++e) dst[e] = from_f32<T>(o[e] * inv);
   }
 }
 

@@ -1,0 +1,252 @@
+"""Process-per-GPU request dispatcher: one request stream served by N B200s.
+
+Requests are independent (reference model/forward.py:186-204), so a box of N
+GPUs serves one stream by routing WHOLE requests to per-GPU worker processes —
+no collective on the scoring path.  Each worker owns one GPU and one
+``DeviceService`` (weights, HBM item table, DSO executors, its own request
+coalescing); the front end, in the caller's process, routes every request to the
+worker with the least outstanding work (the ``sharding.request_work`` rows of the
+requests it holds that have not come back — the online form of
+``assign_requests``), and completes each caller's future when that worker's
+result arrives.  This is the multi-device counterpart of the reference's
+``Service.handle_request`` concurrency (service.py:127-171: a semaphore of
+in-flight requests over one runner; orchestrator.py:163-165: a thread pool of
+chunks).
+
+Transport: one duplex pipe per worker; requests travel as (tag, history ids,
+candidate ids) int64 arrays, results as (tag, scores, compute seconds) — ids,
+not embeddings, cross the process boundary (the feature rows are gathered on the
+worker's GPU).  Inside a worker, a reader thread queues arriving requests and
+two handler threads drain the queue into ``handle_batch`` calls, so one batch
+is staged while the previous one runs on the device.
+
+``scorer_factory(rank)`` builds a worker's scorer (anything with
+``handle_batch(list[ScoreRequest]) -> list[ScoreResponse]`` and ``close()``);
+the default builds ``DeviceService.from_config(config, device=rank)``.
+"""
+
+from __future__ import annotations
+
+import multiprocessing as mp
+import queue
+import threading
+import time
+from concurrent.futures import Future
+
+import numpy as np
+
+from .sharding import request_work
+
+_STOP = "stop"
+
+
+class DispatchError(RuntimeError):
+    """A worker failed to start or died."""
+
+
+class ServiceFactory:
+    """Default worker scorer: a DeviceService on GPU ``rank`` (picklable for spawn)."""
+
+    def __init__(self, config) -> None:
+        self.config = config
+
+    def __call__(self, rank: int):
+        from .service import DeviceService
+
+        return DeviceService.from_config(self.config, device=rank)
+
+
+def _worker_main(rank: int, conn, factory, max_batch: int, handlers: int) -> None:
+    """Worker process: own GPU ``rank``; serve requests from ``conn`` until stopped."""
+    from .service import ScoreRequest
+
+    try:
+        scorer = factory(rank)
+    except BaseException as exc:  # noqa: BLE001 - reported to the front end
+        conn.send(("error", repr(exc)))
+        return
+    conn.send(("ready", rank))
+    inbox: queue.Queue = queue.Queue()
+    send_lock = threading.Lock()
+
+    def handle() -> None:
+        while True:
+            item = inbox.get()
+            if item is None:
+                return
+            batch = [item]
+            while len(batch) < max_batch:
+                try:
+                    nxt = inbox.get_nowait()
+                except queue.Empty:
+                    break
+                if nxt is None:
+                    inbox.put(None)
+                    break
+                batch.append(nxt)
+            reqs = [ScoreRequest(user_id=0, history_item_ids=h, candidate_item_ids=c) for _, h, c in batch]
+            try:
+                out = scorer.handle_batch(reqs)
+                msgs = [("ok", tag, o.scores, o.compute_latency_ms) for (tag, _, _), o in zip(batch, out)]
+            except BaseException as exc:  # noqa: BLE001 - every request of the batch gets it
+                if len(batch) > 1:  # isolate the failing request(s): retry one by one
+                    msgs = []
+                    for tag, r in zip((b[0] for b in batch), reqs):
+                        try:
+                            o = scorer.handle_batch([r])[0]
+                            msgs.append(("ok", tag, o.scores, o.compute_latency_ms))
+                        except BaseException as e1:  # noqa: BLE001
+                            msgs.append(("err", tag, type(e1).__name__, str(e1)))
+                else:
+                    msgs = [("err", batch[0][0], type(exc).__name__, str(exc))]
+            with send_lock:
+                for m in msgs:
+                    conn.send(m)
+
+    threads = [threading.Thread(target=handle, daemon=True) for _ in range(handlers)]
+    for t in threads:
+        t.start()
+    try:
+        while True:
+            msg = conn.recv()
+            if msg == _STOP:
+                break
+            inbox.put(msg)
+    except EOFError:
+        pass
+    for _ in threads:
+        inbox.put(None)
+    for t in threads:
+        t.join()
+    try:
+        scorer.close()
+    finally:
+        with send_lock:
+            conn.send(("closed", rank))
+        conn.close()
+
+
+class MultiDeviceService:
+    """Front end of N per-GPU workers with least-outstanding-work routing."""
+
+    def __init__(self, config=None, n_devices: int = 1, *, scorer_factory=None, max_batch: int = 256,
+                 handlers: int = 2, start_timeout_s: float = 600.0) -> None:
+        if n_devices < 1:
+            raise ValueError("n_devices must be >= 1")
+        if scorer_factory is None:
+            if config is None:
+                raise ValueError("a ServiceConfig or a scorer_factory is required")
+            scorer_factory = ServiceFactory(config)
+        self.num_blocks = config.model.num_blocks if config is not None else 1
+        ctx = mp.get_context("spawn")
+        self._conns, self._procs = [], []
+        for rank in range(n_devices):
+            a, b = ctx.Pipe(duplex=True)
+            p = ctx.Process(target=_worker_main, args=(rank, b, scorer_factory, max_batch, handlers), daemon=True)
+            p.start()
+            b.close()
+            self._conns.append(a)
+            self._procs.append(p)
+        for rank, c in enumerate(self._conns):
+            if not c.poll(start_timeout_s):
+                self._kill()
+                raise DispatchError(f"worker {rank} did not start within {start_timeout_s:.0f}s")
+            msg = c.recv()
+            if msg[0] != "ready":
+                self._kill()
+                raise DispatchError(f"worker {rank} failed to start: {msg[1]}")
+        self.n = n_devices
+        self._lock = threading.Lock()
+        self._send_locks = [threading.Lock() for _ in range(n_devices)]
+        self._outstanding = [0] * n_devices
+        self._pending: dict = {}
+        self._tag = 0
+        self.routed = [0] * n_devices  # requests sent to each worker
+        self._closed = False
+        self._readers = [threading.Thread(target=self._read, args=(r,), daemon=True) for r in range(n_devices)]
+        for t in self._readers:
+            t.start()
+
+    def _kill(self) -> None:
+        for p in self._procs:
+            if p.is_alive():
+                p.kill()
+
+    def _read(self, rank: int) -> None:
+        conn = self._conns[rank]
+        while True:
+            try:
+                msg = conn.recv()
+            except (EOFError, OSError):
+                msg = ("died", rank)
+            if msg[0] in ("closed", "died"):
+                with self._lock:
+                    dead = [t for t, (r, _, _, _) in self._pending.items() if r == rank]
+                    for tag in dead:
+                        _, fut, _, _ = self._pending.pop(tag)
+                        fut.set_exception(DispatchError(f"worker {rank} exited with requests in flight"))
+                return
+            tag = msg[1]
+            with self._lock:
+                r, fut, work, t0 = self._pending.pop(tag)
+                self._outstanding[r] -= work
+            if msg[0] == "ok":
+                fut.set_result((msg[2], msg[3], time.perf_counter() - t0))
+            else:
+                from .service import RequestError
+
+                exc_t = RequestError if msg[2] == "RequestError" else (ValueError if msg[2] == "ValueError"
+                                                                       else RuntimeError)
+                fut.set_exception(exc_t(msg[3]))
+
+    def submit(self, history_item_ids, candidate_item_ids) -> Future:
+        """Route one request; the future yields (scores (C, tasks), compute ms,
+        end-to-end seconds from submit to result)."""
+        h = np.ascontiguousarray(history_item_ids, dtype=np.int64)
+        c = np.ascontiguousarray(candidate_item_ids, dtype=np.int64)
+        work = request_work(h.size, c.size, self.num_blocks)
+        fut: Future = Future()
+        with self._lock:
+            if self._closed:
+                raise RuntimeError("dispatcher is closed")
+            rank = min(range(self.n), key=lambda k: (self._outstanding[k], k))
+            self._outstanding[rank] += work
+            self._tag += 1
+            tag = self._tag
+            self._pending[tag] = (rank, fut, work, time.perf_counter())
+            self.routed[rank] += 1
+        with self._send_locks[rank]:
+            self._conns[rank].send((tag, h, c))
+        return fut
+
+    def score(self, requests) -> list:
+        """Score (history ids, candidate ids) pairs; results in request order."""
+        futs = [self.submit(h, c) for h, c in requests]
+        return [f.result()[0] for f in futs]
+
+    def outstanding(self) -> list:
+        with self._lock:
+            return list(self._outstanding)
+
+    def close(self, timeout_s: float = 60.0) -> None:
+        with self._lock:
+            if self._closed:
+                return
+            self._closed = True
+        for rank, c in enumerate(self._conns):
+            with self._send_locks[rank]:
+                try:
+                    c.send(_STOP)
+                except (BrokenPipeError, OSError):
+                    pass
+        for t in self._readers:
+            t.join(timeout_s)
+        for p in self._procs:
+            p.join(timeout_s)
+        self._kill()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

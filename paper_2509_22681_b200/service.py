@@ -33,9 +33,19 @@ table (off: the host resolves every id from its store copy and ships fp32 rows),
 ``routing`` = ``explicit`` DSO buckets with graphs vs ``implicit`` exact-shape
 executors built per request (reference ``ImplicitShapeRunner``).
 
-Out of scope (host harness without device arithmetic): the host
-feature cache's TTL / staleness modes, simulated store latency, the transfer
-cost model.
+Feature cache.  By default the HBM table is resident and
+always fresh (every id reads the store's current value; ``mutate`` refreshes the
+rows at once).  With ``cache=CacheConfig(...)`` the table becomes the value
+store of the reference's feature cache (``feature_cache.DeviceFeatureCache``,
+cache.py:170-357): it starts cold (zero rows = EMPTY values), every request's
+ids go through the cache's sync single-flight or async stale-while-revalidate
+lookups in the reference's order, fetched values and LRU evictions become row
+writes applied before the batch is submitted, and ``mutate`` only advances the
+store version, so changed features arrive when the TTL expires — the reference
+service's semantics, cold-async zero embeddings included.
+
+Out of scope (host harness without device arithmetic): simulated
+store latency and the transfer cost model.
 """
 
 from __future__ import annotations
@@ -48,6 +58,7 @@ import numpy as np
 
 from .config import ModelConfig
 from .engine import DeviceExecutor, FlameEngine
+from .feature_cache import EMPTY_VALUE, CacheConfig, DeviceFeatureCache
 from .orchestrator import BucketScheduler
 from .params import ModelParams, init_params, load_params
 from .pda import DEFAULT_STORE_SEED, build_item_table, item_embedding
@@ -98,6 +109,8 @@ class ServiceConfig:
     precision: str = "bf16"
     target_rows: int = 16384
     max_batch: int = 256  # requests coalesced into one dispatch
+    cache: CacheConfig | None = None  # reference feature-cache semantics over the table (None: resident)
+    bytes_per_value: int = 512  # store value size (store.py:29), for the fetched-bytes counters
 
     def __post_init__(self) -> None:
         if self.routing not in ROUTINGS:
@@ -117,6 +130,12 @@ class ServiceConfig:
         for k in ("cache_enabled", "mem_opt"):
             if k in d:
                 kw[k] = bool(d[k])
+        if isinstance(d.get("cache"), CacheConfig):
+            kw["cache"] = d["cache"]
+        elif isinstance(d.get("cache"), dict) and d.get("cache_semantics", True):
+            kw["cache"] = CacheConfig.from_dict(d["cache"])
+        if "bytes_per_value" in d.get("remote_store", {}):
+            kw["bytes_per_value"] = int(d["remote_store"]["bytes_per_value"])
         for k in ("num_items", "store_seed", "target_rows", "max_batch"):
             if k in d:
                 kw[k] = int(d[k])
@@ -156,7 +175,8 @@ class DeviceService:
                  store_seed: int = DEFAULT_STORE_SEED, table: np.ndarray | None = None,
                  table_dtype: str = "fp32", precision: str = "bf16", device=None,
                  target_rows: int = 16384, cache_enabled: bool = True, mem_opt: bool = True,
-                 routing: str = "explicit", max_batch: int = 256) -> None:
+                 routing: str = "explicit", max_batch: int = 256, cache: CacheConfig | None = None,
+                 bytes_per_value: int = 512, clock=time.monotonic) -> None:
         if routing not in ROUTINGS:
             raise ValueError(f"routing must be one of {ROUTINGS}, got {routing!r}")
         self.config = config
@@ -170,9 +190,16 @@ class DeviceService:
         # the store's current values; the device table mirrors it (cache on) or
         # the host resolves requests from it (cache off)
         self._store = np.array(table, dtype=np.float32)
-        self.engine.set_table(self._store, dtype=table_dtype)
         self.num_items = self._store.shape[0]
         self._versions: dict[int, int] = {}
+        self.bytes_per_value = bytes_per_value
+        self.feature_cache = None
+        if cache is not None:
+            # the table is the cache's value store: cold = every row EMPTY (zeros)
+            self.feature_cache = DeviceFeatureCache(cache, self._fetch_value, self._decode_value, clock=clock)
+            self.engine.set_table(np.zeros_like(self._store), dtype=table_dtype)
+        else:
+            self.engine.set_table(self._store, dtype=table_dtype)
         self.scheduler = BucketScheduler(self.engine, target_rows=target_rows, with_ids=True, pinned=mem_opt)
         self._lock = threading.Lock()  # device work vs. table refresh
         self._closed = False
@@ -206,7 +233,8 @@ class DeviceService:
         svc = cls(cfg.model, params, num_items=cfg.num_items, store_seed=cfg.store_seed,
                   table_dtype=cfg.table_dtype, precision=cfg.precision, device=device,
                   target_rows=cfg.target_rows, cache_enabled=cfg.cache_enabled, mem_opt=cfg.mem_opt,
-                  routing=cfg.routing, max_batch=cfg.max_batch)
+                  routing=cfg.routing, max_batch=cfg.max_batch, cache=cfg.cache,
+                  bytes_per_value=cfg.bytes_per_value)
         if cfg.profile_shapes:
             svc.warm([(cfg.model.max_history_len, c) for c in cfg.profile_shapes])
         return svc
@@ -351,7 +379,18 @@ class DeviceService:
             self.hits += hits
             self.feature_bytes += nbytes
         order = [i for i, f in enumerate(on_dev) if f] + [i for i, f in enumerate(on_dev) if not f]
+        writes: dict = {}
+        if self.feature_cache is not None:
+            # reference resolve order: per request, history then candidates (service.py:136-137);
+            # the rows each lookup resolved are written before the batch runs
+            for t, f in zip(batch, on_dev):
+                if f:
+                    w = self.feature_cache.lookup_lists((t.hist, t.cand))
+                    if w is not None:
+                        writes.update(zip(w[0].tolist(), w[1]))
         with self._lock:
+            if writes:
+                self._write_rows(writes)
             if self.routing == "explicit":
                 recs = []
                 for work, ids in ((id_work, True), (row_work, False)):
@@ -417,6 +456,33 @@ class DeviceService:
 
     # -- feature path ---------------------------------------------------------
 
+    def _fetch_value(self, item_id: int) -> bytes:
+        """The store's value for an item (store.py:85-102 minus the latency model):
+        the current embedding in the wire format, fp64 LE + filler."""
+        raw = self.embedding_of(item_id).astype("<f8").tobytes()
+        return raw + b"\x00" * max(0, self.bytes_per_value - len(raw))
+
+    def _decode_value(self, value) -> np.ndarray:
+        """store.py:74-78: values shorter than d float64s decode to zeros."""
+        d = self.config.hidden_dim
+        if len(value) < 8 * d:
+            return np.zeros(d, dtype=np.float32)
+        return np.frombuffer(value[: 8 * d], dtype="<f8").astype(np.float32)
+
+    def _write_rows(self, writes: dict) -> None:
+        """Write feature-cache rows {id: row} into the device table (caller holds
+        ``_lock``; waits for the batches on the device first)."""
+        ids = np.fromiter(writes.keys(), dtype=np.int64, count=len(writes))
+        rows = np.stack(list(writes.values())).astype(np.float32, copy=False)
+        self._quiesce()
+        self.engine.update_rows(ids, rows)
+        with self._stats_lock:
+            self.feature_bytes += int(rows.size) * 4
+
+    def cache_stats(self):
+        """Reference Service.cache_stats (service.py:176-177); None without a cache."""
+        return self.feature_cache.stats() if self.feature_cache is not None else None
+
     def embedding_of(self, item_id: int) -> np.ndarray:
         """The store's current embedding of an item (store.py:59-63, any id)."""
         return item_embedding(self.store_seed, int(item_id), self._versions.get(int(item_id), 0),
@@ -433,6 +499,9 @@ class DeviceService:
         with self._lock:
             for i in ids:
                 self._versions[i] = self._versions.get(i, 0) + 1
+            if self.feature_cache is not None:
+                # behind a feature cache the new values arrive through its refreshes
+                return
             tab = sorted({i for i in ids if 0 <= i < self.num_items})
             if not tab:
                 return
@@ -470,11 +539,18 @@ class DeviceService:
             return {"count": len(series), "mean": sum(series) / len(series),
                     "p50": _percentile(series, 0.5), "p99": _percentile(series, 0.99)}
 
+        cache = {"enabled": self.cache_enabled, "lookups": self.lookups,
+                 "hit_rate": self.hits / self.lookups if self.lookups else 0.0}
+        st = self.cache_stats()
+        if st is not None:
+            n = st.hits_fresh + st.hits_stale + st.misses
+            cache.update(hits_fresh=st.hits_fresh, hits_stale=st.hits_stale, misses=st.misses,
+                         remote_queries=st.remote_queries, bytes_fetched=st.bytes_fetched,
+                         hit_rate=(st.hits_fresh + st.hits_stale) / n if n else 0.0)
         with self._stats_lock:
             return {"requests_total": self.requests_total, "pairs_processed": self.pairs_processed,
                     "overall_ms": summary(self._overall_ms), "compute_ms": summary(self._compute_ms),
-                    "cache": {"enabled": self.cache_enabled, "lookups": self.lookups,
-                              "hit_rate": self.hits / self.lookups if self.lookups else 0.0},
+                    "cache": cache,
                     "network_bytes": self.feature_bytes, "dispatches": self.dispatches,
                     "steady_state_allocs": self.steady_state_allocations}
 
@@ -488,5 +564,7 @@ class DeviceService:
                 if remaining <= 0:
                     raise TimeoutError(f"{self._inflight} requests still in flight")
                 self._drained.wait(timeout=remaining)
+        if self.feature_cache is not None:
+            self.feature_cache.close()
         self.scheduler.close()
         self.engine.close()

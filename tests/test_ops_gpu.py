@@ -62,8 +62,20 @@ def test_sumi_attention_operators(gpu, blob, i, prec, tol):
     np.testing.assert_array_equal(full[:, h:], cand)
 
 
-def test_sumi_attention_rejects_wide_heads(gpu):
-    q = np.zeros((1, 4, 128))
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-5), ("bf16", 2e-2)])
+def test_sumi_attention_wide_heads(gpu, prec, tol):
+    # 64 < head_dim <= 128 runs in 128-lane head slots; checked against the oracle
+    # restatement of attention.py:149-178 (pinned to the reference's outputs)
+    from oracle import flame_oracle as orc
+
+    rng = np.random.default_rng(7)
+    for nh, dh, h, c in ((2, 128, 70, 33), (3, 96, 0, 5)):
+        q, k, v = (rng.uniform(-1, 1, (nh, h + c, dh)) for _ in range(3))
+        want = orc.sumi_all(q, k, v, h, 0.8)
+        _close(fb.attention_sumi(q, k, v, h, 0.8, precision=prec), want, tol, f"dh {dh} {prec}")
+        _close(fb.attention_sumi_candidates(q[:, h:], k, v, h, 0.8, precision=prec), want[:, h:], tol,
+               f"dh {dh} candidates {prec}")
+    q = np.zeros((1, 4, 160))
     with pytest.raises(ValueError, match="head_dim"):
         fb.attention_sumi(q, q, q, 2, 1.0)
 

@@ -100,3 +100,14 @@ def test_bench_generator_reproduces_fixture_ids():
     for (h, c), hh, cc in zip(reqs, g["hist_ids"], g["cand_ids"]):
         np.testing.assert_array_equal(h, hh)
         np.testing.assert_array_equal(c, cc)
+
+
+CAP_CASES = ["dh128_l2", "dh96", "dh128_nohist", "tasks12"]
+
+
+@pytest.mark.parametrize("name", CAP_CASES)
+def test_oracle_capability_cases(name):
+    # oracle/gen_golden_caps.py: head_dim 96 / 128 and 12 tasks, from the reference
+    cfg, params, hist, cand, blob = golden_forward(name)
+    assert np.abs(orc.model_forward(hist, cand, params, cfg) - blob["scores"]).max() <= 1e-12
+    assert np.abs(blob["scores"] - blob["sequential"]).max() <= 1e-10

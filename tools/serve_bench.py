@@ -1,0 +1,74 @@
+"""Served-stream throughput and per-request latency through the process-per-GPU
+dispatcher (paper_2509_22681_b200.dispatch.MultiDeviceService).
+
+One request stream (bench.make_requests: Zipf ids over the 100k-item table) is
+routed over N GPU workers, least outstanding work first, with at most
+``--window`` requests in flight.  Per-request latency runs from submit (numpy
+ids in the caller's process) to the scores back in it: IPC to the worker,
+coalescing, staging, H2D, the graph replay, D2H, IPC back.
+
+    python tools/serve_bench.py --workload cfg3 --gpus 1 --requests 2000 --window 256
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from collections import deque
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import bench  # noqa: E402
+from paper_2509_22681_b200.dispatch import MultiDeviceService  # noqa: E402
+from paper_2509_22681_b200.service import ServiceConfig  # noqa: E402
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--requests", type=int, default=2000)
+    ap.add_argument("--window", type=int, default=256)
+    ap.add_argument("--warmup", type=int, default=300)
+    a = ap.parse_args()
+    d, dh, nb, L, f, tasks, H, C, *_ = bench.WORKLOADS[a.workload]
+    cfg = ServiceConfig(model=bench.model_config(a.workload), num_items=bench.NUM_ITEMS,
+                        store_seed=bench.STORE_SEED, target_rows=64 * 512, max_batch=64)
+    reqs = bench.make_requests(a.requests + a.warmup, H, C, bench.WORKLOAD_SEED, a.workload in bench.ZIPF_C)
+    t_start = time.perf_counter()
+    with MultiDeviceService(cfg, n_devices=a.gpus) as svc:
+        startup = time.perf_counter() - t_start
+        for fut in [svc.submit(h, c) for h, c in reqs[: a.warmup]]:
+            fut.result()
+        inflight: deque = deque()
+        lat = []
+        cands = 0
+        t0 = time.perf_counter()
+        for h, c in reqs[a.warmup:]:
+            if len(inflight) >= a.window:
+                s, _, e2e = inflight.popleft().result()
+                lat.append(e2e)
+                cands += s.shape[0]
+            inflight.append(svc.submit(h, c))
+        while inflight:
+            s, _, e2e = inflight.popleft().result()
+            lat.append(e2e)
+            cands += s.shape[0]
+        wall = time.perf_counter() - t0
+        routed = list(svc.routed)
+    lat.sort()
+    line = {"metric": "served candidates/s through the process-per-GPU dispatcher", "workload": a.workload,
+            "n_gpus": a.gpus, "requests": a.requests, "window": a.window, "value": cands / wall,
+            "unit": "candidates/s", "wall_s": wall, "startup_s": startup,
+            "p50_ms": 1000 * bench.nearest_rank(lat, 0.5), "p99_ms": 1000 * bench.nearest_rank(lat, 0.99),
+            "routed_per_gpu": routed,
+            "latency": "submit (numpy ids, caller process) -> scores back in the caller, per request"}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
