@@ -19,7 +19,7 @@ LIB = PKG / "_flame_b200.so"
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-    "-diag-suppress", "177",
+    "-diag-suppress", "177,550",
 ]
 
 

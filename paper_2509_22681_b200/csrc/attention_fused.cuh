@@ -15,9 +15,13 @@
 // blockIdx.x + k * gridDim.x and, inside a unit, PAIRS of 128-row candidate
 // tiles (t0 = 2p, t1 = 2p + 1): warpgroup 0 owns t0, warpgroup 1 owns t1.
 // Both tiles use the same W_{g,h} k-blocks, so one ring stage holds
-//   A_t0 [128 x 64] | A_t1 [128 x 64] | W_q,k,v [192 x 64]   (56 KB)
+//   A_t0 [128 x 32] | A_t1 [128 x 32] | W_q,k,v [192 x 32]   (28 KB, 64-byte swizzle)
 // and feeds two M = 128, N = 192 MMAs (6.7 KB of L2 reads per MFLOP instead of
 // 9.5 for one tile per W load; the K = 512 GEMMs of this pass are L2-bound).
+// The ring holds 4 such 32-deep stages rather than 2 of 64: the same 112 KB, but
+// a slot is refilled as soon as its half-sized stage is consumed, so more bytes
+// are in flight (measured per-stage period at 2 x 64: 1188 cycles for 768 cycles
+// of MMA work, L2-latency-bound).
 // The unit's history K/V (hb <= 256 keys: <= 2 chunks of 128) stays resident
 // for all its pairs and is read from HBM once per (request, block, head).
 //
@@ -65,9 +69,12 @@ constexpr int kKeys = 128;
 constexpr int DH = 64;
 constexpr int kThreads = 352;
 constexpr int kTile = kRows * DH * 2;           // 16 KB: 128 rows x 64 bf16
-constexpr int kWBytes = 3 * DH * DH * 2;        // 24 KB: q | k | v rows of W, 64 k
-constexpr int kStageBytes = 2 * kTile + kWBytes;  // 56 KB
-constexpr int kStages = 2;
+constexpr int kKB = 32;                         // projection k-block depth (64-byte rows)
+constexpr int kATile = kRows * kKB * 2;         // 8 KB: 128 rows x 32 bf16
+constexpr int kWPart = DH * kKB * 2;            // 4 KB: 64 rows of W x 32 bf16
+constexpr int kWBytes = 3 * kWPart;             // 12 KB: q | k | v rows of W, 32 k
+constexpr int kStageBytes = 2 * kATile + kWBytes;  // 28 KB
+constexpr int kStages = 4;
 constexpr int kKOff = kStages * kStageBytes;    // history K chunks [2]
 constexpr int kVOff = kKOff + 2 * kTile;        // history V chunks [2]
 constexpr int kStgOff = kVOff + 2 * kTile;      // per-WG V_self / output staging [2]
@@ -76,15 +83,15 @@ constexpr int kSmemBytes = kBarOff + 256 + 1024;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;
 // barrier slots
-constexpr int RING_FULL = 0, RING_EMPTY = 2, KV_FULL = 4, KV_FREE = 6;
-constexpr int WGB = 7;  // per-WG block of 6: proj_full, q_ready, s_full, s_free, p_full, o_full
+constexpr int RING_FULL = 0, RING_EMPTY = kStages, KV_FULL = 2 * kStages, KV_FREE = 2 * kStages + 2;
+constexpr int WGB = 2 * kStages + 3;  // per-WG block of 6: proj_full, q_ready, s_full, s_free, p_full, o_full
 constexpr int PROJ_FULL = 0, Q_READY = 1, S_FULL = 2, S_FREE = 3, P_FULL = 4, O_FULL = 5;
 constexpr int kBars = WGB + 2 * 6;
 }  // namespace fattn
 
 __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
-    const __grid_constant__ CUtensorMap tm_a,    // Ecc [Rc][D] bf16, box 64 x 128
-    const __grid_constant__ CUtensorMap tm_w,    // Wqkv [G][3DA][D] bf16, box 64 x 64
+    const __grid_constant__ CUtensorMap tm_a,    // Ecc [Rc][D] bf16, box 32 x 128, 64-byte swizzle
+    const __grid_constant__ CUtensorMap tm_w,    // Wqkv [G][3DA][D] bf16, box 32 x 64, 64-byte swizzle
     const __grid_constant__ CUtensorMap tm_qkv,  // QKV [G][rows][3DA] (history K / V), box 64 x 128
     const __grid_constant__ CUtensorMap tm_out,  // AO [G][rows][DA], box 64 x 128
     FusedAttnArgs a) {
@@ -150,6 +157,7 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
     // ------------------------------------------------ A / W ring producer
     const bool leader = ptx::elect_one();
     uint32_t rk = 0;
+    unsigned trace_k = 0;
     for (int k = 0;; ++k) {
       const Unit un = unit_at(k);
       if (!un.valid) break;
@@ -160,16 +168,17 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
         for (int kb = 0; kb < KB; ++kb, ++rk) {
           const int s = rk % kStages;
           if (rk >= kStages) ptx::mbar_wait(bars + RING_EMPTY + s, ((rk / kStages) - 1) & 1);
+          ATTN_TRACE(3, 21);
           if (leader) {
             uint8_t* st = smem + s * kStageBytes;
             uint64_t* fb = bars + RING_FULL + s;
-            ptx::mbar_arrive_expect_tx(fb, (has1 ? 2 : 1) * kTile + kWBytes);
-            ptx::tma_load_3d(st, &tm_a, fb, kb * 64, arow, 0);
-            if (has1) ptx::tma_load_3d(st + kTile, &tm_a, fb, kb * 64, arow + kRows, 0);
-            uint8_t* w = st + 2 * kTile;
-            ptx::tma_load_3d(w, &tm_w, fb, kb * 64, un.h * DH, un.g);
-            ptx::tma_load_3d(w + DH * 128, &tm_w, fb, kb * 64, a.DA + un.h * DH, un.g);
-            ptx::tma_load_3d(w + 2 * DH * 128, &tm_w, fb, kb * 64, 2 * a.DA + un.h * DH, un.g);
+            ptx::mbar_arrive_expect_tx(fb, (has1 ? 2 : 1) * kATile + kWBytes);
+            ptx::tma_load_3d(st, &tm_a, fb, kb * kKB, arow, 0);
+            if (has1) ptx::tma_load_3d(st + kATile, &tm_a, fb, kb * kKB, arow + kRows, 0);
+            uint8_t* w = st + 2 * kATile;
+            ptx::tma_load_3d(w, &tm_w, fb, kb * kKB, un.h * DH, un.g);
+            ptx::tma_load_3d(w + kWPart, &tm_w, fb, kb * kKB, a.DA + un.h * DH, un.g);
+            ptx::tma_load_3d(w + 2 * kWPart, &tm_w, fb, kb * kKB, 2 * a.DA + un.h * DH, un.g);
           }
           __syncwarp();
         }
@@ -204,6 +213,7 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
     constexpr uint32_t idesc_o = ptx::make_idesc_bf16(kRows, DH, 0, 1);
     uint32_t rk = 0, ku = 0;
     uint32_t nj[2] = {0, 0}, cc[2] = {0, 0};
+    unsigned trace_k = 0;
     for (int k = 0;; ++k) {
       const Unit un = unit_at(k);
       if (!un.valid) break;
@@ -215,16 +225,17 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
         for (int kb = 0; kb < KB; ++kb, ++rk) {
           const int s = rk % kStages;
           ptx::mbar_wait(bars + RING_FULL + s, (rk / kStages) & 1);
+          ATTN_TRACE(2, 31);
           ptx::tc_fence_after();
           if (leader) {
             const uint32_t st = ptx::smem_u32(smem + s * kStageBytes);
-            const uint32_t aw = st + 2 * kTile;
+            const uint32_t aw = st + 2 * kATile;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t bd = ptx::make_desc_sw128(aw + kk * 32, 16, 1024);
-              ptx::mma_bf16_ss(tmem, ptx::make_desc_sw128(st + kk * 32, 16, 1024), bd, idesc_p, (kb | kk) != 0);
+            for (int kk = 0; kk < kKB / 16; ++kk) {
+              const uint64_t bd = ptx::make_desc_sw64(aw + kk * 32, 512);
+              ptx::mma_bf16_ss(tmem, ptx::make_desc_sw64(st + kk * 32, 512), bd, idesc_p, (kb | kk) != 0);
               if (has1)
-                ptx::mma_bf16_ss(tmem + 256, ptx::make_desc_sw128(st + kTile + kk * 32, 16, 1024), bd, idesc_p,
+                ptx::mma_bf16_ss(tmem + 256, ptx::make_desc_sw64(st + kATile + kk * 32, 512), bd, idesc_p,
                                  (kb | kk) != 0);
             }
             ptx::mma_commit(bars + RING_EMPTY + s);
@@ -237,7 +248,9 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
         }
         __syncwarp();
         // the warpgroups read q / k / v and stored Q (bf16) into TMEM
+        ATTN_TRACE(2, 32);
         for (int i = 0; i < nw; ++i) ptx::mbar_wait(WB(i, Q_READY), nj[i] & 1);
+        ATTN_TRACE(2, 33);
         if (un.nk > 0) {
           auto issue_s = [&](int i, int c) {
             if (p == 0) ptx::mbar_wait(bars + KV_FULL + c, ku & 1);  // first use of chunk c in this unit
@@ -274,6 +287,7 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
             }
             for (int i = 0; i < nw; ++i) {
               ptx::mbar_wait(WB(i, P_FULL), cc[i] & 1);  // P_c stored (and O rescaled)
+              ATTN_TRACE(2, 35);
               ptx::tc_fence_after();
               const uint32_t aV = ptx::smem_u32(smem + kVOff + c * kTile);
               const uint32_t tP = tmem + i * 256 + 128, tO = tmem + i * 256 + 192;
@@ -307,6 +321,7 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
     uint8_t* stage = smem + kStgOff + i * kTile;
     uint32_t nj = 0, cc = 0;
     bool store_pending = false;
+    unsigned trace_k = 0;
     for (int k = 0;; ++k) {
       const Unit un = unit_at(k);
       if (!un.valid) break;
@@ -321,6 +336,7 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
         const bool row_ok = t * kRows + row < min(__ldg(a.cand_len + un.r), a.c_bkt);
         const float rs = row_ok ? __ldg(a.rs_c + cidx) : 0.f;
         ptx::mbar_wait(WB(i, PROJ_FULL), nj & 1);
+        ATTN_TRACE(i, 41);
         ptx::tc_fence_after();
         // ---- projection epilogue: q = rs * acc + c_q (folded LN1), same for k, v
         float dot = 0.f;
@@ -348,6 +364,12 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
           }
           ptx::tmem_st_32x32b_x16(tQ + half * 16, qb);
         }
+        // Q is in TMEM: the S MMAs may start (they overwrite q | k, columns [0, 128);
+        // v, read below, lives in [128, 192), which only this warpgroup's P overwrites)
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(WB(i, Q_READY));
+        ATTN_TRACE(i, 42);
         // V_self rows -> the staging tile (bf16, SW128 row layout); the previous
         // job's output store must have finished reading the staging first
         if (store_pending) {
@@ -373,9 +395,6 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
             *reinterpret_cast<uint4*>(stage + ptx::sw128_offset(row, (half * 32 + e) * 2)) = w;
           }
         }
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(WB(i, Q_READY));
         // the diagonal of the SUMI mask seeds the state: m = s_self, l = 1 (attention.py:134)
         const float m_self = dot * sl2;
         float m = m_self, l = 1.f;
@@ -383,6 +402,7 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
           const int key_lim = un.hb - c * kKeys;
           const bool full = __all_sync(0xffffffffu, key_lim >= kKeys);
           ptx::mbar_wait(WB(i, S_FULL), cc & 1);
+          ATTN_TRACE(i, 43);
           ptx::tc_fence_after();
           uint32_t s[kKeys];
 #pragma unroll
@@ -456,11 +476,13 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
           ptx::tmem_st_wait();
           ptx::tc_fence_before();
           ptx::mbar_arrive(WB(i, P_FULL));
+          ATTN_TRACE(i, 44);
         }
         // out = (O + exp2(s_self - m) v_self) / l; H = 0 gives out = v_self
         float o[DH];
         if (un.nk > 0) {
           ptx::mbar_wait(WB(i, O_FULL), (cc - 1) & 1);
+          ATTN_TRACE(i, 45);
           ptx::tc_fence_after();
           uint32_t ov[DH];
 #pragma unroll
@@ -522,6 +544,7 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
           // every row read its V_self before any row's next-job epilogue rewrites the staging
           asm volatile("bar.sync %0, 128;" ::"r"(1 + i) : "memory");
         }
+        ATTN_TRACE(i, 46);
         ++nj;
       }
     }

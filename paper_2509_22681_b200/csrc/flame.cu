@@ -657,12 +657,14 @@ struct Pipe {
     fa.out = static_cast<__nv_bfloat16*>(e->AO);
     fa.out_ld = DA; fa.out_gstride = e->rows * static_cast<long long>(DA);
     fa.DA = DA; fa.nh = c->nh; fa.R = e->R; fa.hb_bkt = e->hb_bkt; fa.c_bkt = e->c_bkt; fa.num_blocks = G;
-    fa.k_blocks = D / 64; fa.hist_len = e->io.hist_len; fa.cand_len = e->io.cand_len;
+    fa.k_blocks = D / fattn::kKB; fa.hist_len = e->io.hist_len; fa.cand_len = e->io.cand_len;
     fa.scale_log2 = c->scale_log2; fa.rs_c = e->rs_c; fa.cqkv = w.cqkv;
     fa.store_tma = (e->c_bkt % 128) == 0; fa.active = e->io.active;
     CUtensorMap ta, tw, tq, to;
-    if (!make_tmap_bf16_3d(&ta, e->Ecc, D, e->Rc, 1, static_cast<uint64_t>(D) * 2, 0, 64, 128) ||
-        !make_tmap_bf16_3d(&tw, w.wqkv, D, 3ULL * DA, G, static_cast<uint64_t>(D) * 2, 3ULL * DA * D * 2, 64, 64) ||
+    if (!make_tmap_bf16_3d_swz(&ta, e->Ecc, D, e->Rc, 1, static_cast<uint64_t>(D) * 2, 0, fattn::kKB, 128,
+                               CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !make_tmap_bf16_3d_swz(&tw, w.wqkv, D, 3ULL * DA, G, static_cast<uint64_t>(D) * 2, 3ULL * DA * D * 2,
+                               fattn::kKB, 64, CU_TENSOR_MAP_SWIZZLE_64B) ||
         !make_tmap_bf16_3d(&tq, e->QKV, 3ULL * DA, e->rows, G, 3ULL * DA * 2, e->rows * 3ULL * DA * 2, 64, 128) ||
         !make_tmap_bf16_3d(&to, e->AO, DA, e->rows, G, static_cast<uint64_t>(DA) * 2,
                            e->rows * static_cast<uint64_t>(DA) * 2, 64, 128))

@@ -365,6 +365,18 @@ __device__ __forceinline__ uint64_t make_desc_sw128(uint32_t smem_addr, uint32_t
   return d;
 }
 
+// Same for a 64-byte-swizzled K-major tile (rows of 64 bytes = 32 bf16; atoms
+// of 8 rows x 64 B = 512 B): layout type 4 (SWIZZLE_64B).
+__device__ __forceinline__ uint64_t make_desc_sw64(uint32_t smem_addr, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;  // LBO: unused for swizzled K-major layouts
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;
+  return d;
+}
+
 // Instruction descriptor for kind::f16: bf16 x bf16 -> fp32.
 // [4,6) c_format (1 = F32), [7,10) a_format (1 = BF16), [10,13) b_format,
 // [15] a_major, [16] b_major (0 = K, 1 = MN), [17,23) N>>3, [24,29) M>>4.

@@ -23,11 +23,13 @@ inline PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 // 3-D bf16 tensor map [groups][rows][inner] with a (box_inner x box_rows x 1)
-// box and 128-byte swizzle (box_inner * 2 must be <= 128).  Out-of-bounds
+// box and 128-byte swizzle (box_inner * 2 must be <= 128), or the 64-byte one
+// (box_inner * 2 <= 64) when asked.  Out-of-bounds
 // elements read as zero, which is what pads ragged M / N tiles.
-inline bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
-                              uint64_t groups, uint64_t row_stride_bytes,
-                              uint64_t group_stride_bytes, uint32_t box_inner, uint32_t box_rows) {
+inline bool make_tmap_bf16_3d_swz(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
+                                  uint64_t groups, uint64_t row_stride_bytes,
+                                  uint64_t group_stride_bytes, uint32_t box_inner, uint32_t box_rows,
+                                  CUtensorMapSwizzle swizzle) {
   auto fn = get_encode_fn();
   if (!fn) return false;
   std::memset(map, 0, sizeof(*map));
@@ -39,9 +41,16 @@ inline bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t inner
   cuuint32_t box[3] = {box_inner, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+inline bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
+                              uint64_t groups, uint64_t row_stride_bytes,
+                              uint64_t group_stride_bytes, uint32_t box_inner, uint32_t box_rows) {
+  return make_tmap_bf16_3d_swz(map, base, inner, rows, groups, row_stride_bytes, group_stride_bytes, box_inner,
+                               box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 // Same for fp32 operands (the tf32 GEMM): box_inner * 4 <= 128.
