@@ -323,9 +323,11 @@ def choose_peak(tensor: bool, clk: dict | None) -> tuple[float, str]:
     if not tensor:
         return peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]), f"{src} (hbm_gbs)"
     burst = bool(clk and clk.get("sm_mhz") and clk.get("sm_max_mhz")
-                 and clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"] and "sw_power_cap" not in clk.get("reasons", []))
+                 and clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"]
+                 and not {"sw_power_cap", "after-load"} & set(clk.get("reasons", [])))
     key = "bf16_tflops" if burst else "bf16_tflops_sustained"
-    why = "profile-pass SM clock at max, no power cap" if burst else "profile-pass SM clock below max or power-capped"
+    why = ("profile-pass SM clock at max, no power cap" if burst
+           else "profile-pass SM clock below max, power-capped, or right after sustained load")
     return peaks.get(key, FALLBACK_PEAKS[key]), f"{src} ({key}: {why})"
 
 
@@ -421,6 +423,40 @@ def cpu_baseline_line(args, dist, name: str):
                       f"p99 {1000 * nearest_rank(r['lat'], 0.99):.0f} ms"}
 
 
+def fp32_verify_line(eng, params, cfg, reqs, R, C, dev, step_flops, steps: int = 3) -> dict:
+    """The same step in the fp32 verification mode (true-fp32 SIMT GEMMs and
+    attention, the north star's <= 1e-4 mode): device-timed cand/s over a few
+    graph replays, and the largest |fp32 - bf16| score difference on the batch."""
+    import torch
+
+    import paper_2509_22681_b200 as fb
+    from paper_2509_22681_b200 import _lib
+    from paper_2509_22681_b200.pda import build_item_table
+
+    e32 = fb.FlameEngine(params, cfg, precision="fp32", device=dev.index)
+    try:
+        e32.set_table(build_item_table(NUM_ITEMS, cfg.hidden_dim, STORE_SEED), dtype="fp32")
+        ex32 = e32.executor(R, cfg.max_history_len // cfg.num_blocks, C, with_ids=True)
+        s32 = ex32.score_ids(reqs)
+        s16 = eng.executor(R, cfg.max_history_len // cfg.num_blocks, C, with_ids=True).score_ids(reqs)
+        diff = max(float(np.abs(a - b).max()) for a, b in zip(s32, s16))
+        ex32.stage_ids(reqs)
+        ex32.run(_lib.INPUT_IDS, graph=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.stream(ex32.stream):
+            ev[0].record(ex32.stream)
+            for _ in range(steps):
+                ex32.run(_lib.INPUT_IDS, graph=True)
+            ev[1].record(ex32.stream)
+        ex32.stream.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / steps
+    finally:
+        e32.close()
+    return {"value": R * C / (ms / 1e3), "unit": "candidates/s", "ms_per_step": ms, "steps": steps,
+            "tflops": round(step_flops / (ms / 1e3) / 1e12, 1), "max_abs_vs_bf16": diff,
+            "kernels": "fp32 FFMA SIMT GEMMs + fp32 SUMI attention (precision='fp32')"}
+
+
 def run_ours(args, dist) -> None:
     import torch
 
@@ -443,6 +479,13 @@ def run_ours(args, dist) -> None:
     ex.run(_lib.INPUT_IDS, graph=True)  # capture + first replay
     ex.stream.synchronize()
     launches = ex.launch_count()
+
+    # --------------------------------------------------- roofline (live)
+    # eager per-launch CUDA events with their own clock record, BEFORE the timed
+    # region: the kernels timed alone, at burst clocks (after sustained load the
+    # power-capped state stretches the L2-bound kernels by up to 30 %,
+    # dev/prof_ab.py; that state is reported separately as roofline.hot)
+    prof, prof_clk = profile_pass(ex, _lib.INPUT_IDS, 5, dev.index)
 
     # ---------------------------------------------------- device-timed region
     for _ in range(args.warmup):
@@ -471,13 +514,16 @@ def run_ours(args, dist) -> None:
     cands = R * C * args.steps * dist.world_size
     value = cands / (total_ms / 1e3)
 
-    # --------------------------------------------------- roofline (live)
-    # eager per-launch CUDA events, before the long e2e region (so its clocks are
-    # not the power-capped tail of it), with its own clock record
-    prof, prof_clk = profile_pass(ex, _lib.INPUT_IDS, 5, dev.index)
     pda = pda_algorithmic_bytes(ex, d, 4)
     tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels = roofline(
         prof, name, prof_clk, {k: pda[k] for k in ("pda_dedup", "pda_gather")})
+    # the same profile right after the timed region (the hot state of the step)
+    prof_hot, hot_clk = profile_pass(ex, _lib.INPUT_IDS, 5, dev.index)
+    h = roofline(prof_hot, name, hot_clk, {k: pda[k] for k in ("pda_dedup", "pda_gather")})
+    hot_peak, hot_src = choose_peak(h[0], {**(hot_clk or {}), "reasons": ["after-load"]})
+    hot = {"kernel": h[1], "avg_launch_ms": h[7], "achieved": round(h[2], 1), "peak": hot_peak,
+           "frac": round(h[2] / hot_peak, 4), "peak_source": hot_src + " (after the timed region)",
+           "clocks": hot_clk, "step_sum_ms": round(sum(v["ms_per_step"] for v in h[8].values()), 4)}
 
     # -------------------------------------------------------------- e2e
     # through the public streaming API: numpy ids in, numpy scores out, every step
@@ -511,12 +557,15 @@ def run_ours(args, dist) -> None:
     step_flops = algorithmic_flops(cfg, H, C) * R
     step_tf = step_flops / (sum(step_ms) / args.steps / 1e3) / 1e12
 
+    # ------------------------------------------ fp32 verification mode
+    fp32 = None if args.no_fp32_line else fp32_verify_line(eng, params, cfg, reqs, R, C, dev, step_flops)
+
     # ------------------------------------------------------ CPU baseline
     cpu_baseline = cpu_baseline_line(args, dist, name)
 
     emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf, e2e_value, e2e_steps,
               h2d, d2h, launches, tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels, clk,
-              cpu_baseline, prof_clk=prof_clk, pda=pda, e2e_lat=(e2e_p50, e2e_p99))
+              cpu_baseline, prof_clk=prof_clk, pda=pda, e2e_lat=(e2e_p50, e2e_p99), fp32=fp32, hot=hot)
 
 
 def run_dso(args, dist) -> None:
@@ -666,7 +715,8 @@ def e2e_step_count(args, step_ms) -> int:
 
 def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99, step_tf, e2e_value, e2e_steps,
               h2d, d2h, launches, tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels, clk,
-              cpu_baseline, extra_config=None, e2e_path=None, latency_note=None, prof_clk=None, pda=None, e2e_lat=None):
+              cpu_baseline, extra_config=None, e2e_path=None, latency_note=None, prof_clk=None, pda=None, e2e_lat=None,
+              fp32=None, hot=None):
     if dist.rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": dist.world_size,
@@ -701,8 +751,10 @@ def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99
                          "traffic": traffic,
                          "peak_source": peak_src,
                          "per_launch": per_launch, "avg_launch_ms": avg_ms,
-                         "timing": "per-launch CUDA events on the executor stream, eager profile pass run "
-                                   "before the e2e region",
+                         "timing": "per-launch CUDA events on the executor stream, eager pass enqueued behind "
+                                   "a gate kernel (launches back to back), median of 5, run before the timed "
+                                   "region (kernels timed alone)",
+                         **({"hot": hot} if hot else {}),
                          "profile_clocks": prof_clk,
                          "traffic_source": "profiles/ncu_dram_per_launch.json (ncu --set full of tools/prof_step.py: "
                                            "the bench's own workload, 100k-item fp32 table)"},
@@ -712,6 +764,8 @@ def emit_line(args, dist, name, desc, R, C, H, nb, d, L, f, value, total_ms, p99
             "clocks": clk,
             "cpu_baseline": cpu_baseline,
         }
+        if fp32:
+            line["fp32_verify"] = fp32
         if extra_config:
             line["config"].update(extra_config)
         print(json.dumps(line), flush=True)
@@ -725,6 +779,7 @@ def main() -> None:
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--requests", type=int, default=0, help="requests per step per GPU (0 = default)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-fp32-line", action="store_true", help="skip the fp32 verification-mode line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -13,10 +13,11 @@ result arrives.  This is the multi-device counterpart of the reference's
 in-flight requests over one runner; orchestrator.py:163-165: a thread pool of
 chunks).
 
-Transport: one duplex pipe per worker; requests travel as (tag, history ids,
-candidate ids) int64 arrays, results as (tag, scores, compute seconds) — ids,
-not embeddings, cross the process boundary (the feature rows are gathered on the
-worker's GPU).  Inside a worker, a reader thread queues arriving requests and
+Transport: one duplex pipe per worker; a group of requests travels as one frame
+(tags, per-request lengths, and the concatenated history / candidate ids as
+int64 arrays), a scored batch comes back as one message (tags, row counts, the
+concatenated score rows, compute times) — ids, not embeddings, cross the process
+boundary (the feature rows are gathered on the worker's GPU).  Inside a worker, a reader thread queues arriving requests and
 two handler threads drain the queue into ``handle_batch`` calls, so one batch
 is staged while the previous one runs on the device.
 
@@ -87,7 +88,11 @@ def _worker_main(rank: int, conn, factory, max_batch: int, handlers: int) -> Non
             reqs = [ScoreRequest(user_id=0, history_item_ids=h, candidate_item_ids=c) for _, h, c in batch]
             try:
                 out = scorer.handle_batch(reqs)
-                msgs = [("ok", tag, o.scores, o.compute_latency_ms) for (tag, _, _), o in zip(batch, out)]
+                # one message for the whole batch: tags, per-request row counts, all score rows
+                msgs = [("oks", np.array([b[0] for b in batch], dtype=np.int64),
+                         np.array([o.scores.shape[0] for o in out], dtype=np.int64),
+                         np.concatenate([o.scores for o in out]),
+                         np.array([o.compute_latency_ms for o in out]))]
             except BaseException as exc:  # noqa: BLE001 - every request of the batch gets it
                 if len(batch) > 1:  # isolate the failing request(s): retry one by one
                     msgs = []
@@ -111,7 +116,14 @@ def _worker_main(rank: int, conn, factory, max_batch: int, handlers: int) -> Non
             msg = conn.recv()
             if msg == _STOP:
                 break
-            inbox.put(msg)
+            if msg[0] == "frame":  # several requests in one message (submit_many)
+                _, tags, hl, cl, hflat, cflat = msg
+                hs = np.split(hflat, np.cumsum(hl)[:-1])
+                cs = np.split(cflat, np.cumsum(cl)[:-1])
+                for tag, h, c in zip(tags.tolist(), hs, cs):
+                    inbox.put((tag, h, c))
+            else:
+                inbox.put(msg)
     except EOFError:
         pass
     for _ in threads:
@@ -186,6 +198,19 @@ class MultiDeviceService:
                         _, fut, _, _ = self._pending.pop(tag)
                         fut.set_exception(DispatchError(f"worker {rank} exited with requests in flight"))
                 return
+            if msg[0] == "oks":
+                _, tags, counts, flat, ms = msg
+                now = time.perf_counter()
+                rows = np.split(flat, np.cumsum(counts)[:-1])
+                done = []
+                with self._lock:
+                    for tag in tags.tolist():
+                        r, fut, work, t0 = self._pending.pop(tag)
+                        self._outstanding[r] -= work
+                        done.append((fut, t0))
+                for (fut, t0), sc, m in zip(done, rows, ms.tolist()):
+                    fut.set_result((sc, m, now - t0))
+                continue
             tag = msg[1]
             with self._lock:
                 r, fut, work, t0 = self._pending.pop(tag)
@@ -202,26 +227,41 @@ class MultiDeviceService:
     def submit(self, history_item_ids, candidate_item_ids) -> Future:
         """Route one request; the future yields (scores (C, tasks), compute ms,
         end-to-end seconds from submit to result)."""
-        h = np.ascontiguousarray(history_item_ids, dtype=np.int64)
-        c = np.ascontiguousarray(candidate_item_ids, dtype=np.int64)
-        work = request_work(h.size, c.size, self.num_blocks)
-        fut: Future = Future()
+        return self.submit_many([(history_item_ids, candidate_item_ids)])[0]
+
+    def submit_many(self, requests) -> list:
+        """Route a group of requests, each to the worker with the least outstanding
+        work at its turn, and send each worker its share as ONE message (ids
+        concatenated); returns one future per request, in order."""
+        hs = [np.ascontiguousarray(h, dtype=np.int64).reshape(-1) for h, _ in requests]
+        cs = [np.ascontiguousarray(c, dtype=np.int64).reshape(-1) for _, c in requests]
+        futs = [Future() for _ in requests]
+        per: dict = {}
+        t0 = time.perf_counter()
         with self._lock:
             if self._closed:
                 raise RuntimeError("dispatcher is closed")
-            rank = min(range(self.n), key=lambda k: (self._outstanding[k], k))
-            self._outstanding[rank] += work
-            self._tag += 1
-            tag = self._tag
-            self._pending[tag] = (rank, fut, work, time.perf_counter())
-            self.routed[rank] += 1
-        with self._send_locks[rank]:
-            self._conns[rank].send((tag, h, c))
-        return fut
+            for k, (h, c) in enumerate(zip(hs, cs)):
+                work = request_work(h.size, c.size, self.num_blocks)
+                rank = min(range(self.n), key=lambda q: (self._outstanding[q], q))
+                self._outstanding[rank] += work
+                self._tag += 1
+                self._pending[self._tag] = (rank, futs[k], work, t0)
+                self.routed[rank] += 1
+                per.setdefault(rank, []).append((self._tag, k))
+        for rank, items in per.items():
+            tags = np.array([t for t, _ in items], dtype=np.int64)
+            idx = [k for _, k in items]
+            msg = ("frame", tags, np.array([hs[k].size for k in idx], dtype=np.int64),
+                   np.array([cs[k].size for k in idx], dtype=np.int64),
+                   np.concatenate([hs[k] for k in idx]), np.concatenate([cs[k] for k in idx]))
+            with self._send_locks[rank]:
+                self._conns[rank].send(msg)
+        return futs
 
     def score(self, requests) -> list:
         """Score (history ids, candidate ids) pairs; results in request order."""
-        futs = [self.submit(h, c) for h, c in requests]
+        futs = self.submit_many(list(requests))
         return [f.result()[0] for f in futs]
 
     def outstanding(self) -> list:

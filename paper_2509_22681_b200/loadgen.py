@@ -17,7 +17,10 @@ What the columns measure here:
   requests are coalesced into DSO batches by the service;
 * ``compute_ms_*`` — dispatch to collection of the request's group on the GPU;
 * ``cache_hit_rate`` — share of ids served by the HBM item table (0 with
-  ``cache`` off, when the host resolves every id from its store copy);
+  ``cache`` off, when the host resolves every id from its store copy); with a
+  ``cache`` section in the service config the table runs the reference's cache
+  semantics (``feature_cache.py``) and the rate is the reference's
+  (fresh + stale hits) / lookups;
 * ``network_bytes`` — feature bytes moved host -> device in the run (8 B per
   id with the device table, 4·d B per id without, plus row refreshes);
 * ``steady_state_allocs`` — executor buffers allocated after startup (0 for

@@ -3,7 +3,8 @@ dispatcher (paper_2509_22681_b200.dispatch.MultiDeviceService).
 
 One request stream (bench.make_requests: Zipf ids over the 100k-item table) is
 routed over N GPU workers, least outstanding work first, with at most
-``--window`` requests in flight.  Per-request latency runs from submit (numpy
+``--window`` requests in flight, submitted in frames of ``--frame`` requests
+(``submit_many``: one message per worker per frame).  Per-request latency runs from submit (numpy
 ids in the caller's process) to the scores back in it: IPC to the worker,
 coalescing, staging, H2D, the graph replay, D2H, IPC back.
 
@@ -34,6 +35,7 @@ def main() -> None:
     ap.add_argument("--requests", type=int, default=2000)
     ap.add_argument("--window", type=int, default=256)
     ap.add_argument("--warmup", type=int, default=300)
+    ap.add_argument("--frame", type=int, default=16, help="requests per submit_many call (one message per worker)")
     a = ap.parse_args()
     d, dh, nb, L, f, tasks, H, C, *_ = bench.WORKLOADS[a.workload]
     cfg = ServiceConfig(model=bench.model_config(a.workload), num_items=bench.NUM_ITEMS,
@@ -42,18 +44,19 @@ def main() -> None:
     t_start = time.perf_counter()
     with MultiDeviceService(cfg, n_devices=a.gpus) as svc:
         startup = time.perf_counter() - t_start
-        for fut in [svc.submit(h, c) for h, c in reqs[: a.warmup]]:
+        for fut in svc.submit_many(reqs[: a.warmup]):
             fut.result()
         inflight: deque = deque()
         lat = []
         cands = 0
         t0 = time.perf_counter()
-        for h, c in reqs[a.warmup:]:
-            if len(inflight) >= a.window:
+        body = reqs[a.warmup:]
+        for f0 in range(0, len(body), a.frame):
+            while len(inflight) >= a.window:
                 s, _, e2e = inflight.popleft().result()
                 lat.append(e2e)
                 cands += s.shape[0]
-            inflight.append(svc.submit(h, c))
+            inflight.extend(svc.submit_many(body[f0:f0 + a.frame]))
         while inflight:
             s, _, e2e = inflight.popleft().result()
             lat.append(e2e)
@@ -62,7 +65,7 @@ def main() -> None:
         routed = list(svc.routed)
     lat.sort()
     line = {"metric": "served candidates/s through the process-per-GPU dispatcher", "workload": a.workload,
-            "n_gpus": a.gpus, "requests": a.requests, "window": a.window, "value": cands / wall,
+            "n_gpus": a.gpus, "requests": a.requests, "window": a.window, "frame": a.frame, "value": cands / wall,
             "unit": "candidates/s", "wall_s": wall, "startup_s": startup,
             "p50_ms": 1000 * bench.nearest_rank(lat, 0.5), "p99_ms": 1000 * bench.nearest_rank(lat, 0.99),
             "routed_per_gpu": routed,
