@@ -16,9 +16,12 @@ one CUDA graph.  Metric: candidates scored / s (whole job, all ranks).
 * ``e2e``    the same metric through the public API (``DeviceExecutor.score_ids``):
   host ids -> pinned staging -> H2D -> forward -> D2H scores -> numpy, per step.
 * ``roofline`` the dominant kernel, timed live with per-launch CUDA events in
-  an eager profiling pass; FLOPs are algorithmic.
-* ``cpu_baseline`` the numpy oracle port of the reference (oracle/) on this
-  host's cores (rank 0, N = 1 only), a bounded sample of the same workload.
+  an eager profiling pass before the timed region (``roofline.hot``: the same
+  right after it); FLOPs are algorithmic.
+* ``fp32_verify`` the same step in the fp32 verification mode.
+* ``cpu_baseline`` the unmodified reference (installed in baseline/_ref) on
+  this host's cores — or, without that install, the numpy oracle port of it
+  (oracle/) — rank 0, N = 1 only, a bounded sample of the same workload.
 * ``--impl reference`` times that CPU reference path alone (rank 0; other
   ranks exit without work).
 
@@ -614,6 +617,29 @@ def run_dso(args, dist) -> None:
         groups.append(ex)
     torch.cuda.synchronize()
     launches = sum(ex.launch_count() for ex in groups)
+    # per-launch profile before the timed region (kernels timed alone, as in run_ours)
+    clocks_p = ClockSampler(dev.index, period_s=0.002)
+    clocks_p.start()
+    clocks_p.begin()
+    # each group's launch marks count its full bucket (slots x c_bkt rows); the
+    # kernels skip unused slots and padded candidate rows, so scale every record to
+    # the group's REAL rows: history-row kernels by active / slots, candidate-row
+    # kernels by sum(C_i) / (slots x c_bkt)
+    ratios = []
+    for (hb, cb), idx in plan:
+        slots = sched.slots_for(cb)
+        ratios.append((len(idx) / slots, sum(counts[i] for i in idx) / (slots * cb)))
+
+    def scaled(recs, rh, rc):
+        out = []
+        for rec in recs:
+            k = rh if "hist" in rec["name"] else rc
+            out.append({**rec, "flops": rec["flops"] * k, "bytes": rec["bytes"] * k})
+        return out
+
+    prof = [[rec for ex, (rh, rc) in zip(groups, ratios) for rec in scaled(ex.profile(_lib.INPUT_IDS), rh, rc)]
+            for _ in range(2)]
+    prof_clk = clocks_p.stop()
     main = torch.cuda.Stream(device=dev)
 
     def step(ev_start, ev_end):
@@ -649,11 +675,6 @@ def run_dso(args, dist) -> None:
     total_ms = dist.max(sum(step_ms))
     value = n_cand * args.steps * dist.world_size / (total_ms / 1e3)
 
-    clocks_p = ClockSampler(dev.index, period_s=0.002)
-    clocks_p.start()
-    clocks_p.begin()
-    prof = [[rec for ex in groups for rec in ex.profile(_lib.INPUT_IDS)] for _ in range(2)]
-    prof_clk = clocks_p.stop()
     pdas = [pda_algorithmic_bytes(ex, d, 4) for ex in groups]
     pda = {k: sum(p[k] for p in pdas) for k in pdas[0]}
     tensor, top, achieved, peak, traffic, peak_src, per_launch, avg_ms, kernels = roofline(
