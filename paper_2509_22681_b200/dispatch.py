@@ -174,6 +174,10 @@ class MultiDeviceService:
         self._pending: dict = {}
         self._tag = 0
         self.routed = [0] * n_devices  # requests sent to each worker
+        self._stats_lock = threading.Lock()
+        self._overall_ms: list = []
+        self._compute_ms: list = []
+        self.pairs_processed = 0
         self._closed = False
         self._readers = [threading.Thread(target=self._read, args=(r,), daemon=True) for r in range(n_devices)]
         for t in self._readers:
@@ -240,7 +244,9 @@ class MultiDeviceService:
         t0 = time.perf_counter()
         with self._lock:
             if self._closed:
-                raise RuntimeError("dispatcher is closed")
+                from .service import ServiceClosedError
+
+                raise ServiceClosedError("dispatcher is closed")
             for k, (h, c) in enumerate(zip(hs, cs)):
                 work = request_work(h.size, c.size, self.num_blocks)
                 rank = min(range(self.n), key=lambda q: (self._outstanding[q], q))
@@ -263,6 +269,45 @@ class MultiDeviceService:
         """Score (history ids, candidate ids) pairs; results in request order."""
         futs = self.submit_many(list(requests))
         return [f.result()[0] for f in futs]
+
+    # -- the DeviceService request interface (so api.create_app can serve N GPUs)
+    def handle_batch(self, reqs) -> list:
+        """Reference ``Service.handle_request`` semantics for a list of
+        ``ScoreRequest``s, routed over the workers: ``ScoreResponse``s in order;
+        contract violations raise the workers' ``RequestError``."""
+        from .service import ScoreResponse
+
+        t0 = time.perf_counter()
+        futs = self.submit_many([(r.history_item_ids, r.candidate_item_ids) for r in reqs])
+        out = []
+        for f in futs:
+            scores, compute_ms, _ = f.result()
+            out.append(ScoreResponse(scores, (time.perf_counter() - t0) * 1000.0, compute_ms))
+        with self._stats_lock:
+            for o in out:
+                self._overall_ms.append(o.overall_latency_ms)
+                self._compute_ms.append(o.compute_latency_ms)
+                self.pairs_processed += o.scores.shape[0]
+        return out
+
+    def handle_request(self, req):
+        return self.handle_batch([req])[0]
+
+    def metrics_snapshot(self) -> dict:
+        """Front-end view: request counts, latency summaries (nearest rank), the
+        requests routed to each GPU worker."""
+        from .service import _percentile
+
+        def summary(series):
+            if not series:
+                return {"count": 0}
+            return {"count": len(series), "mean": sum(series) / len(series),
+                    "p50": _percentile(series, 0.5), "p99": _percentile(series, 0.99)}
+
+        with self._stats_lock:
+            return {"requests_total": len(self._overall_ms), "pairs_processed": self.pairs_processed,
+                    "overall_ms": summary(self._overall_ms), "compute_ms": summary(self._compute_ms),
+                    "routed_per_worker": list(self.routed), "workers": self.n}
 
     def outstanding(self) -> list:
         with self._lock:

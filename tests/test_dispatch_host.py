@@ -100,3 +100,19 @@ def test_closed_dispatcher_refuses():
     s.close()
     with pytest.raises(RuntimeError):
         s.submit(np.zeros(2, dtype=np.int64), np.arange(2))
+
+
+def test_http_over_the_dispatcher(svc):
+    # api.create_app serves the dispatcher like a DeviceService (N GPUs behind one HTTP front end)
+    from fastapi.testclient import TestClient
+
+    from paper_2509_22681_b200.api import create_app
+
+    app = create_app(svc)
+    client = TestClient(app)  # no context manager: the fixture owns the dispatcher's lifetime
+    r = client.post("/score", json={"user_id": 1, "history": [1, 2, 3, 4], "candidates": [10, 11]})
+    assert r.status_code == 200
+    assert [row[0] for row in r.json()["scores"]] == [24.0, 26.0]
+    assert client.post("/score", json={"user_id": 1, "history": [1], "candidates": []}).status_code == 400
+    m = client.get("/metrics").json()
+    assert m["requests_total"] >= 1 and m["workers"] == 2
