@@ -154,6 +154,7 @@ struct FlameCtx {
 struct FlameExec {
   FlameCtx* ctx = nullptr;
   int R = 0, hb_bkt = 0, c_bkt = 0, H_bkt = 0, cap = 0;
+  int nseg = 1;  // PDA segments per id list (lists longer than kPdaMaxList ids)
   long long Rh = 0, Rc = 0, rows = 0;
   FlameIO io{};
   float* Eh = nullptr;
@@ -715,14 +716,19 @@ struct Pipe {
     l.hist_ids = e->io.hist_ids; l.cand_ids = e->io.cand_ids;
     l.hist_len = e->io.hist_len; l.cand_len = e->io.cand_len;
     l.R = e->R; l.H_bkt = e->H_bkt; l.C_bkt = e->c_bkt;
-    l.unique = e->io.unique_ids ? e->io.unique_ids : e->unique_ws;
-    l.inverse = e->io.inverse ? e->io.inverse : e->inverse_ws;
-    l.n_unique = e->io.n_unique ? e->io.n_unique : e->nuniq_ws;
-    l.spos = e->spos; l.ustart = e->ustart; l.cap = e->cap; l.active = e->io.active;
+    // segmented lists (nseg > 1) keep their per-segment maps in the workspace: the
+    // caller's [2R][capacity] buffers hold whole-list np.unique maps only
+    const bool own_maps = e->nseg == 1;
+    if (mode == FLAME_INPUT_GATHER_ONLY && !own_maps)
+      return fail(1, "np.unique maps of id lists longer than " + std::to_string(kPdaMaxList) + " ids are not produced");
+    l.unique = own_maps && e->io.unique_ids ? e->io.unique_ids : e->unique_ws;
+    l.inverse = own_maps && e->io.inverse ? e->io.inverse : e->inverse_ws;
+    l.n_unique = own_maps && e->io.n_unique ? e->io.n_unique : e->nuniq_ws;
+    l.spos = e->spos; l.ustart = e->ustart; l.cap = e->cap; l.nseg = e->nseg; l.active = e->io.active;
     l.work = e->work; l.n_work = e->n_work; l.wcap = e->wcap;
     // dedup: one CTA per list, radix sort sized to the list capacity
     mark("pda_dedup", 0.0, static_cast<double>(e->R) * (e->H_bkt + e->c_bkt) * (8.0 + 8.0 + 8.0 + 8.0));
-    if (int rc = launch_dedup(l, e->cap, 2 * e->R, s)) return rc;
+    if (int rc = launch_dedup(l, e->cap, 2 * e->R * e->nseg, s)) return rc;
     if (int rc = check()) return rc;
     {
       PdaGatherArgs g{};
@@ -730,7 +736,7 @@ struct Pipe {
       g.hb_bkt = e->hb_bkt; g.o = assemble_out();
       // one warp per work item (a <= 32-position piece of a unique id's run) plus one
       // per padding row (together <= wcap); up to 4 of them per warp
-      dim3 grid(static_cast<unsigned>((e->wcap + 31) / 32), 2 * e->R);
+      dim3 grid(static_cast<unsigned>((e->wcap + 31) / 32), 2 * e->R * e->nseg);
       // rows out + table rows read (upper bound: one per position); candidates also get fp32
       const double tab = c->table_dtype == FLAME_TABLE_BF16 ? 2.0 : 4.0;
       mark("pda_gather", 0.0, static_cast<double>(e->R) * c->D *
@@ -1184,12 +1190,14 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
   if (R < 1 || hb_bkt < 0 || c_bkt < 1) return fail(1, "bad executor shape");
   if (static_cast<long long>(hb_bkt) * c->G > c->cfg.max_history_len)
     return fail(1, "executor history capacity exceeds max_history_len");
-  const int cap = flame_exec_list_capacity(c->G, hb_bkt, c_bkt);
-  if (cap > kPdaMaxList) return fail(1, "id list longer than the PDA dedup kernel supports");
+  // id lists longer than one dedup CTA's kPdaMaxList are split into segments
+  const int cap_full = flame_exec_list_capacity(c->G, hb_bkt, c_bkt);
+  const int nseg = (cap_full + kPdaMaxList - 1) / kPdaMaxList;
+  const int cap = cap_full < kPdaMaxList ? cap_full : kPdaMaxList;
   CUDA_TRY(cudaSetDevice(c->device));
   auto* e = new FlameExec();
   e->ctx = c;
-  e->R = R; e->hb_bkt = hb_bkt; e->c_bkt = c_bkt; e->H_bkt = hb_bkt * c->G; e->cap = cap;
+  e->R = R; e->hb_bkt = hb_bkt; e->c_bkt = c_bkt; e->H_bkt = hb_bkt * c->G; e->cap = cap; e->nseg = nseg;
   e->Rh = static_cast<long long>(R) * hb_bkt;
   e->Rc = static_cast<long long>(R) * c_bkt;
   e->rows = e->Rh + e->Rc;
@@ -1226,14 +1234,15 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
   e->Xb = c->L > 1 ? static_cast<float*>(A(G * rows * D * 4)) : nullptr;
   e->Fz = A(e->Rc * D * 4);  // fp32 fused rows (both modes)
   e->He = (fold && c->tasks <= 4) ? nullptr : A(e->Rc * F * 4);
-  e->spos = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
-  e->ustart = static_cast<int*>(A(2 * static_cast<size_t>(R) * cap * 4));
+  const size_t lists = 2 * static_cast<size_t>(R) * nseg;  // (list, segment) slots
+  e->spos = static_cast<int*>(A(lists * cap * 4));
+  e->ustart = static_cast<int*>(A(lists * cap * 4));
   e->wcap = cap + cap / kRunPiece + 1;
-  e->work = static_cast<int2*>(A(2 * static_cast<size_t>(R) * e->wcap * 8));
-  e->n_work = static_cast<int*>(A(2 * static_cast<size_t>(R) * 4));
-  e->unique_ws = static_cast<long long*>(A(2 * static_cast<size_t>(R) * cap * 8));
-  e->inverse_ws = static_cast<long long*>(A(2 * static_cast<size_t>(R) * cap * 8));
-  e->nuniq_ws = static_cast<int*>(A(2 * static_cast<size_t>(R) * 4));
+  e->work = static_cast<int2*>(A(lists * e->wcap * 8));
+  e->n_work = static_cast<int*>(A(lists * 4));
+  e->unique_ws = static_cast<long long*>(A(lists * cap * 8));
+  e->inverse_ws = static_cast<long long*>(A(lists * cap * 8));
+  e->nuniq_ws = static_cast<int*>(A(lists * 4));
   if (!ok) {
     delete e;
     return fail(2, "executor workspace allocation failed");

@@ -25,7 +25,7 @@
 namespace flame {
 
 constexpr int kRunPiece = 32;  // positions one gather warp writes per work item
-constexpr int kPdaMaxList = 8192;  // ids per list handled by one CTA (cfg5: 8184)
+constexpr int kPdaMaxList = 8192;  // ids per list SEGMENT handled by one CTA (cfg5: 8184 = one segment)
 
 struct PdaLists {
   const long long* hist_ids;  // [R][H_bkt]
@@ -33,17 +33,22 @@ struct PdaLists {
   const int* hist_len;        // [R]
   const int* cand_len;        // [R]
   int R, H_bkt, C_bkt;
-  // outputs (list l = r for history, R + r for candidates; row stride = list capacity)
-  long long* unique;   // [2R][cap]
-  long long* inverse;  // [2R][cap]
-  int* n_unique;       // [2R]
-  int* spos;           // [2R][cap] positions in sorted order
-  int* ustart;         // [2R][cap] run start (index into spos) of each unique id
-  int2* work;          // [2R][wcap] gather work items (unique index, first sorted position):
+  // outputs, per list SEGMENT L = list * nseg + s (list = r for history, R + r for
+  // candidates; segment s holds list positions [s * cap, (s + 1) * cap)); a list
+  // longer than kPdaMaxList ids is deduplicated segment by segment (its rows are
+  // still exact: a duplicate across segments is only gathered twice), so the
+  // np.unique maps below are per segment, and exactly np.unique's when nseg == 1
+  long long* unique;   // [2R * nseg][cap]
+  long long* inverse;  // [2R * nseg][cap] (segment-local positions)
+  int* n_unique;       // [2R * nseg]
+  int* spos;           // [2R * nseg][cap] segment-local positions in sorted order
+  int* ustart;         // [2R * nseg][cap] run start (index into spos) of each unique id
+  int2* work;          // [2R * nseg][wcap] gather work items (unique index, first sorted position):
                        // each unique id's run split into pieces of <= kRunPiece positions
-  int* n_work;         // [2R]
+  int* n_work;         // [2R * nseg]
   int wcap;            // cap + cap / kRunPiece + 1
-  int cap;             // max(H_bkt, C_bkt)
+  int cap;             // ids per segment: min(max(H_bkt, C_bkt), kPdaMaxList)
+  int nseg;            // segments per list
   const int* active;   // [1] requests in use (null: all R); lists of unused slots are skipped
 };
 
@@ -57,19 +62,22 @@ __global__ void __launch_bounds__(kThreads) pda_dedup(PdaLists a) {
   using Sort = cub::BlockRadixSort<unsigned long long, kThreads, kItems, int>;
   constexpr int P = kThreads * kItems;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int list = blockIdx.x;
+  const int seg_list = blockIdx.x;  // output slot of this (list, segment)
+  const int list = seg_list / a.nseg, seg = seg_list % a.nseg;
   const bool is_hist = list < a.R;
   const int r = is_hist ? list : list - a.R;
   if (a.active != nullptr && r >= __ldg(a.active)) {
     if (threadIdx.x == 0) {
-      a.n_unique[list] = 0;
-      a.n_work[list] = 0;
+      a.n_unique[seg_list] = 0;
+      a.n_work[seg_list] = 0;
     }
     return;
   }
-  const int n = is_hist ? a.hist_len[r] : a.cand_len[r];
-  const long long* ids = is_hist ? a.hist_ids + static_cast<long long>(r) * a.H_bkt
-                                 : a.cand_ids + static_cast<long long>(r) * a.C_bkt;
+  const int n_list = is_hist ? a.hist_len[r] : a.cand_len[r];
+  const int n = max(0, min(a.cap, n_list - seg * a.cap));  // ids of this segment
+  const long long* ids = (is_hist ? a.hist_ids + static_cast<long long>(r) * a.H_bkt
+                                  : a.cand_ids + static_cast<long long>(r) * a.C_bkt) +
+                         static_cast<long long>(seg) * a.cap;
   __shared__ unsigned long long s_max;
   __shared__ int warp_tot[32];
   if (threadIdx.x == 0) s_max = 0;
@@ -140,10 +148,10 @@ __global__ void __launch_bounds__(kThreads) pda_dedup(PdaLists a) {
   }
   __syncthreads();
   const int offset = (incl - local) + (w > 0 ? warp_tot[w - 1] : 0);
-  long long* uq = a.unique + static_cast<long long>(list) * a.cap;
-  long long* inv = a.inverse + static_cast<long long>(list) * a.cap;
-  int* sp = a.spos + static_cast<long long>(list) * a.cap;
-  int* us = a.ustart + static_cast<long long>(list) * a.cap;
+  long long* uq = a.unique + static_cast<long long>(seg_list) * a.cap;
+  long long* inv = a.inverse + static_cast<long long>(seg_list) * a.cap;
+  int* sp = a.spos + static_cast<long long>(seg_list) * a.cap;
+  int* us = a.ustart + static_cast<long long>(seg_list) * a.cap;
   int first_rk[kItems];  // unique index of this thread's run starts (-1: not a start)
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) pda_dedup(PdaLists a) {
       sp[i] = pos[i];
     }
   }
-  if (threadIdx.x == blockDim.x - 1) a.n_unique[list] = offset + local;
+  if (threadIdx.x == blockDim.x - 1) a.n_unique[seg_list] = offset + local;
 
   // gather work list: a Zipf-hot id's run (hundreds of positions) would otherwise
   // be written by one warp while the rest of the grid idles; cut every run into
@@ -206,14 +214,14 @@ __global__ void __launch_bounds__(kThreads) pda_dedup(PdaLists a) {
   }
   __syncthreads();
   int woff = (pincl - plocal) + (w > 0 ? warp_tot[w - 1] : 0);
-  int2* wk = a.work + static_cast<long long>(list) * a.wcap;
+  int2* wk = a.work + static_cast<long long>(seg_list) * a.wcap;
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
     const int rk = threadIdx.x * kItems + k;
     for (int c = 0; c < pcs[k]; ++c) wk[woff + c] = make_int2(rk, rs[rk] + c * kRunPiece);
     woff += pcs[k];
   }
-  if (threadIdx.x == blockDim.x - 1) a.n_work[list] = woff;
+  if (threadIdx.x == blockDim.x - 1) a.n_work[seg_list] = woff;
 }
 
 template <typename TTab>
@@ -268,20 +276,25 @@ __device__ __forceinline__ void assemble_row_st(const AssembleOut& o, bool hist,
 // resident CTAs per SM: the kernel is memory-latency bound.
 template <typename TTab, int kChunks>
 __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
-  const int list = blockIdx.y;
+  const int seg_list = blockIdx.y;  // (list, segment) of pda_dedup
+  const int list = seg_list / a.l.nseg, seg = seg_list % a.l.nseg;
   const bool is_hist = list < a.l.R;
   const int r = is_hist ? list : list - a.l.R;
   if (a.l.active != nullptr && r >= __ldg(a.l.active)) return;  // unused slot: its rows are never read
   const int n = is_hist ? a.l.hist_len[r] : a.l.cand_len[r];
-  const int nu = a.l.n_unique[list];
-  const int nw = a.l.n_work[list];
+  const int n_seg = max(0, min(a.l.cap, n - seg * a.l.cap));  // positions of this segment
+  const int p0 = seg * a.l.cap;                               // first list position of the segment
+  const int nu = a.l.n_unique[seg_list];
+  const int nw = a.l.n_work[seg_list];
   const int lane = threadIdx.x % 32;
   const int hb = is_hist ? n / a.G : 0;
-  const int pad_rows = is_hist ? a.G * (a.hb_bkt - hb) : (a.l.C_bkt - n);
+  // the list's padding rows are zeroed by its first segment's warps
+  const int pad_rows = seg != 0 ? 0 : (is_hist ? a.G * (a.hb_bkt - hb) : (a.l.C_bkt - n));
   const int work = nw + pad_rows;
   const int stride = gridDim.x * (blockDim.x / 32);
   for (int u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; u < work; u += stride) {
-  auto row_of = [&](int p) -> long long {  // destination row of list position p
+  auto row_of = [&](int q) -> long long {  // destination row of segment position q
+    const int p = p0 + q;
     if (is_hist) {
       const int g = p / hb, i = p % hb;
       return static_cast<long long>(g) * a.l.R * a.hb_bkt + static_cast<long long>(r) * a.hb_bkt + i;
@@ -290,13 +303,13 @@ __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
   };
   if (u < nw) {
     // one piece (<= kRunPiece positions) of one unique id's run
-    const long long* uq = a.l.unique + static_cast<long long>(list) * a.l.cap;
-    const int* sp = a.l.spos + static_cast<long long>(list) * a.l.cap;
-    const int* us = a.l.ustart + static_cast<long long>(list) * a.l.cap;
-    const int2 wi = a.l.work[static_cast<long long>(list) * a.l.wcap + u];
+    const long long* uq = a.l.unique + static_cast<long long>(seg_list) * a.l.cap;
+    const int* sp = a.l.spos + static_cast<long long>(seg_list) * a.l.cap;
+    const int* us = a.l.ustart + static_cast<long long>(seg_list) * a.l.cap;
+    const int2 wi = a.l.work[static_cast<long long>(seg_list) * a.l.wcap + u];
     const long long id = uq[wi.x];
     const int b = wi.y;
-    const int e = min(b + kRunPiece, (wi.x + 1 < nu) ? us[wi.x + 1] : n);
+    const int e = min(b + kRunPiece, (wi.x + 1 < nu) ? us[wi.x + 1] : n_seg);
     const bool known = id >= 0 && id < a.num_items;
     const TTab* table = reinterpret_cast<const TTab*>(a.table) + (known ? id : 0) * a.D;
     float4 v[kChunks];

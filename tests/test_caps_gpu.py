@@ -33,3 +33,28 @@ def test_capability_single_candidate_rows_bit_exact(gpu, name):
     for i in range(3):
         np.testing.assert_array_equal(fb.model_forward(hist, cand[i:i + 1], params, cfg, precision="fp32")[0],
                                       full[i])
+
+
+@pytest.mark.parametrize("nb,H", [(1, 20000), (4, 17000 - 17000 % 4)])
+def test_long_id_lists_are_deduplicated_in_segments(gpu, nb, H):
+    # history id lists longer than one dedup CTA's 8192 ids are split into
+    # segments (a duplicate across segments is only gathered twice): the scores
+    # equal the oracle's on the rows the reference store resolves
+    from oracle import flame_oracle as orc
+    from paper_2509_22681_b200.pda import build_item_table
+
+    cfg = fb.ModelConfig(64, 16, nb, 1, 128, 2, H, 64, seed=9)
+    params = fb.init_params(cfg)
+    table = build_item_table(3000, 64)
+    eng = fb.FlameEngine(params, cfg, precision="fp32")
+    try:
+        eng.set_table(table, dtype="fp32")
+        rng = np.random.default_rng(5)
+        hist = (rng.zipf(1.3, H) % 3000).astype(np.int64)  # many repeats, across segments too
+        cand = rng.integers(0, 3000, 37)
+        ex = eng.executor(1, H // nb, 64, with_ids=True)
+        got = ex.score_ids([(hist, cand)])[0]
+        want = orc.model_forward(table[hist].astype(np.float64), table[cand].astype(np.float64), params, cfg)
+        assert np.abs(got - want).max() <= 1e-4
+    finally:
+        eng.close()
