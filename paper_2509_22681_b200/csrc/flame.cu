@@ -429,7 +429,7 @@ int validate_desc(const FlameModelDesc& m) {
   if (m.hidden_dim % m.head_dim != 0) return fail(1, "head_dim must divide hidden_dim");
   if (m.max_history_len % m.num_blocks != 0) return fail(1, "num_blocks must divide max_history_len");
   if (m.head_dim > 128) return fail(1, "head_dim > 128 is not supported by the attention kernels");
-  if (pad_to(m.hidden_dim, 64) > 1024 || m.hidden_dim / m.head_dim * (m.head_dim <= 64 ? 64 : 128) > 4096)
+  if (pad_to(m.hidden_dim, 64) > 2048 || m.hidden_dim / m.head_dim * (m.head_dim <= 64 ? 64 : 128) > 4096)
     return fail(1, "hidden_dim too large for the row kernels");
   return 0;
 }
@@ -562,7 +562,11 @@ struct Pipe {
     const int threads = 256;
     dim3 grid(static_cast<unsigned>((rows * 32 + threads - 1) / threads), c->G);
     mark("layer_norm", 0.0, static_cast<double>(c->G) * rows * c->D * (4.0 + sizeof(Act)));
-    layer_norm_rows<Act><<<grid, threads, 0, s>>>(src, src_ld, src_gstride, out, out_ld, out_gstride,
+    if (c->D > 1024)
+      layer_norm_rows<Act, 16><<<grid, threads, 0, s>>>(src, src_ld, src_gstride, out, out_ld, out_gstride,
+                                                        gamma, beta, static_cast<int>(rows), c->D, c->d);
+    else
+      layer_norm_rows<Act><<<grid, threads, 0, s>>>(src, src_ld, src_gstride, out, out_ld, out_gstride,
                                                   gamma, beta, static_cast<int>(rows), c->D, c->d);
     return check();
   }
@@ -705,9 +709,15 @@ struct Pipe {
       const long long warps = static_cast<long long>(c->G) * e->Rh + e->Rc;
       const int threads = 256;
       mark("scatter_embeddings", 0.0, static_cast<double>(warps) * (c->d * 4.0 + c->D * (row_bytes + 4.0)));
-      scatter_embeddings<<<static_cast<unsigned>((warps * 32 + threads - 1) / threads), threads, 0, s>>>(
-          e->io.hist_emb, e->io.cand_emb, c->d, c->D, e->R, e->H_bkt, e->c_bkt, c->G, e->hb_bkt,
-          e->io.hist_len, e->io.cand_len, assemble_out());
+      const unsigned blocks = static_cast<unsigned>((warps * 32 + threads - 1) / threads);
+      if (c->D > 1024)
+        scatter_embeddings<16><<<blocks, threads, 0, s>>>(e->io.hist_emb, e->io.cand_emb, c->d, c->D, e->R, e->H_bkt,
+                                                          e->c_bkt, c->G, e->hb_bkt, e->io.hist_len, e->io.cand_len,
+                                                          assemble_out());
+      else
+        scatter_embeddings<8><<<blocks, threads, 0, s>>>(e->io.hist_emb, e->io.cand_emb, c->d, c->D, e->R, e->H_bkt,
+                                                         e->c_bkt, c->G, e->hb_bkt, e->io.hist_len, e->io.cand_len,
+                                                         assemble_out());
       return check();
     }
     if (!e->io.hist_ids || !e->io.cand_ids) return fail(1, "id inputs not bound");
@@ -749,7 +759,9 @@ struct Pipe {
     case 2: PDA_GATHER(T, 2); break;                                      \
     case 3: case 4: PDA_GATHER(T, 4); break;                              \
     case 5: case 6: PDA_GATHER(T, 6); break;                              \
-    default: PDA_GATHER(T, 8); break;                                     \
+    case 7: case 8: PDA_GATHER(T, 8); break;                              \
+    case 9: case 10: case 11: case 12: PDA_GATHER(T, 12); break;          \
+    default: PDA_GATHER(T, 16); break;                                    \
   }
       if (c->table_dtype == FLAME_TABLE_BF16) {
         PDA_GATHER_T(__nv_bfloat16)

@@ -27,12 +27,11 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a,
 // deviations, (x - mean) / sqrt(var + 1e-5) * scale + shift.  Statistics run
 // over the first d_true columns; padded columns have scale = shift = 0 and
 // come out as 0.  One warp per row; rows of group g use gamma/beta of block g.
-template <typename TOut>
+template <typename TOut, int kMaxPerLane = 8>  // float4 chunks per lane: D <= 32*4*kMaxPerLane
 __global__ void layer_norm_rows(const float* __restrict__ src, long long src_ld,
                                 long long src_gstride, TOut* __restrict__ out, long long out_ld,
                                 long long out_gstride, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, int rows, int D, int d_true) {
-  constexpr int kMaxPerLane = 8;  // float4 chunks per lane: D <= 32*4*8 = 1024
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   const int g = blockIdx.y;
@@ -244,25 +243,27 @@ struct AssembleOut {
   float* rs_c;               // [R*c_bkt]
 };
 
-__device__ __forceinline__ void assemble_row(const AssembleOut& o, bool hist, long long row, const float4 (&v)[8],
-                                             int lane, int D, int d_true, bool valid) {
+template <int kChunks>
+__device__ __forceinline__ void assemble_row(const AssembleOut& o, bool hist, long long row,
+                                             const float4 (&v)[kChunks], int lane, int D, int d_true, bool valid) {
   float* f = hist ? o.Eh : o.Ec;
   if (f != nullptr) {
     float* dst = f + row * D;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < kChunks; ++k) {
       const int c = (k * 32 + lane) * 4;
       if (c < D) *reinterpret_cast<float4*>(dst + c) = v[k];
     }
   }
   __nv_bfloat16* y = hist ? o.Ehc : o.Ecc;
   if (y != nullptr) {
-    const RowStats st = valid ? warp_row_stats<8>(v, lane, D, d_true) : RowStats{0.f, 0.f};
-    store_centered<8>(y + row * D, v, st.mean, lane, D, d_true);
+    const RowStats st = valid ? warp_row_stats<kChunks>(v, lane, D, d_true) : RowStats{0.f, 0.f};
+    store_centered<kChunks>(y + row * D, v, st.mean, lane, D, d_true);
     if (lane == 0) (hist ? o.rs_h : o.rs_c)[row] = st.rstd;
   }
 }
 
+template <int kChunks>  // float4 chunks per lane: D <= 128 * kChunks
 __global__ void scatter_embeddings(const float* __restrict__ hist, const float* __restrict__ cand,
                                    int d, int D, int R, int H_bkt, int C_bkt, int G, int hb_bkt,
                                    const int* __restrict__ hist_len, const int* __restrict__ cand_len,
@@ -288,16 +289,16 @@ __global__ void scatter_embeddings(const float* __restrict__ hist, const float* 
     const int r = static_cast<int>(row / C_bkt), c = static_cast<int>(row % C_bkt);
     if (c < cand_len[r]) src = cand + row * d;
   }
-  float4 v[8];
+  float4 v[kChunks];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < kChunks; ++k) {
     const int c = (k * 32 + lane) * 4;
     float e[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) e[q] = (src != nullptr && c + q < d) ? src[c + q] : 0.f;
     v[k] = make_float4(e[0], e[1], e[2], e[3]);
   }
-  assemble_row(o, is_hist, row, v, lane, D, d, src != nullptr);
+  assemble_row<kChunks>(o, is_hist, row, v, lane, D, d, src != nullptr);
 }
 
 }  // namespace flame

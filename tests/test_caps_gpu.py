@@ -16,7 +16,7 @@ TOL = {"fp32": 1e-4, "bf16": 2e-2}
 
 
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
-@pytest.mark.parametrize("name", ["dh128_l2", "dh96", "dh128_nohist", "tasks12"])
+@pytest.mark.parametrize("name", ["dh128_l2", "dh96", "dh128_nohist", "tasks12", "d1536"])
 def test_capability_forward_matches_reference(gpu, name, prec):
     cfg, params, hist, cand, blob = golden_forward(name)
     out = fb.model_forward(hist, cand, params, cfg, precision=prec)

@@ -102,7 +102,7 @@ def test_bench_generator_reproduces_fixture_ids():
         np.testing.assert_array_equal(c, cc)
 
 
-CAP_CASES = ["dh128_l2", "dh96", "dh128_nohist", "tasks12"]
+CAP_CASES = ["dh128_l2", "dh96", "dh128_nohist", "tasks12", "d1536"]
 
 
 @pytest.mark.parametrize("name", CAP_CASES)
