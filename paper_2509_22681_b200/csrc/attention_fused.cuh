@@ -247,26 +247,27 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
           if (has1) ptx::mma_commit(WB(1, PROJ_FULL));
         }
         __syncwarp();
-        // the warpgroups read q / k / v and stored Q (bf16) into TMEM
+        // each warpgroup stored its Q (bf16) into TMEM: its first S MMA starts at once
         ATTN_TRACE(2, 32);
-        for (int i = 0; i < nw; ++i) ptx::mbar_wait(WB(i, Q_READY), nj[i] & 1);
+        auto issue_s = [&](int i, int c) {
+          if (p == 0) ptx::mbar_wait(bars + KV_FULL + c, ku & 1);  // first use of chunk c in this unit
+          ptx::tc_fence_after();
+          const uint32_t aK = ptx::smem_u32(smem + kKOff + c * kTile);
+          const uint32_t tS = tmem + i * 256, tQ = tS + 192;
+          if (leader) {
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk)
+              ptx::mma_bf16_ts(tS, tQ + kk * 8, ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
+            ptx::mma_commit(WB(i, S_FULL));
+          }
+          __syncwarp();
+        };
+        for (int i = 0; i < nw; ++i) {
+          ptx::mbar_wait(WB(i, Q_READY), nj[i] & 1);
+          if (un.nk > 0) issue_s(i, 0);
+        }
         ATTN_TRACE(2, 33);
         if (un.nk > 0) {
-          auto issue_s = [&](int i, int c) {
-            if (p == 0) ptx::mbar_wait(bars + KV_FULL + c, ku & 1);  // first use of chunk c in this unit
-            ptx::tc_fence_after();
-            const uint32_t aK = ptx::smem_u32(smem + kKOff + c * kTile);
-            const uint32_t tS = tmem + i * 256, tQ = tS + 192;
-            if (leader) {
-#pragma unroll
-              for (int kk = 0; kk < DH / 16; ++kk)
-                ptx::mma_bf16_ts(tS, tQ + kk * 8, ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
-              ptx::mma_commit(WB(i, S_FULL));
-            }
-            __syncwarp();
-          };
-          issue_s(0, 0);
-          if (has1) issue_s(1, 0);
           for (int c = 0; c < un.nk; ++c) {
             for (int i = 0; i < nw; ++i) {
               ptx::mbar_wait(WB(i, S_FREE), cc[i] & 1);  // S_c in the WG's registers
@@ -365,10 +366,14 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
           ptx::tmem_st_32x32b_x16(tQ + half * 16, qb);
         }
         // Q is in TMEM: the S MMAs may start (they overwrite q | k, columns [0, 128);
-        // v, read below, lives in [128, 192), which only this warpgroup's P overwrites)
+        // v, read below, lives in [128, 192), which only this warpgroup's P
+        // overwrites).  Without history there is no S / P: the next projection
+        // (all of [0, 192)) is what follows Q_READY, so v must be read first.
         ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(WB(i, Q_READY));
+        if (un.nk > 0) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(WB(i, Q_READY));
+        }
         ATTN_TRACE(i, 42);
         // V_self rows -> the staging tile (bf16, SW128 row layout); the previous
         // job's output store must have finished reading the staging first
@@ -394,6 +399,10 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
             w.w = pack_bf16x2(fmaf(rs, __uint_as_float(va[e + 6]), b1.z), fmaf(rs, __uint_as_float(va[e + 7]), b1.w));
             *reinterpret_cast<uint4*>(stage + ptx::sw128_offset(row, (half * 32 + e) * 2)) = w;
           }
+        }
+        if (un.nk == 0) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(WB(i, Q_READY));
         }
         // the diagonal of the SUMI mask seeds the state: m = s_self, l = 1 (attention.py:134)
         const float m_self = dot * sl2;

@@ -177,3 +177,20 @@ def test_full_size_batch_invariance_cfg3_ids(gpu):
         np.testing.assert_array_equal(a, b)
     np.testing.assert_array_equal(full[0], full[6])
     assert all(np.isfinite(s).all() and s.shape == (len(c), 2) for (_, c), s in zip(reqs, full))
+
+
+def test_batch_with_empty_and_full_histories_matches_oracle(gpu):
+    # many units per CTA (R * G * heads > 148) and several tile pairs per unit, with
+    # requests without history (out = v_self, no S / P phase) mixed in: the fused
+    # kernel's epilogue must not release the projection accumulator early
+    from oracle import flame_oracle as orc
+
+    cfg = fb.ModelConfig(128, 64, 2, 1, 256, 2, 256, 512, seed=4)
+    params = fb.init_params(cfg)
+    rng = np.random.default_rng(12)
+    reqs = [(rng.uniform(-1, 1, ((0 if i % 3 else 256), 128)), rng.uniform(-1, 1, (300 + i, 128))) for i in range(64)]
+    outs = fb.model_forward_batch(reqs, params, cfg)
+    for (h, c), o in zip(reqs[:12], outs[:12]):
+        assert np.abs(o - orc.model_forward(h, c, params, cfg)).max() <= 2e-2
+    for (h, c), o in zip(reqs, outs):  # batch composition invariance, bit for bit
+        np.testing.assert_array_equal(o, fb.model_forward(h, c, params, cfg))
