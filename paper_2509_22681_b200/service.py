@@ -427,10 +427,13 @@ class DeviceService:
             batch[i].scores, batch[i].lat = s_, l_
 
     def _quiesce(self) -> None:
-        """Wait until no batch is on the device (caller holds ``_lock``, so no
-        new batch can be submitted)."""
-        with self._cv:
-            self._cv.wait_for(lambda: self._on_device == 0)
+        """Wait until the device has finished every submitted batch (caller holds
+        ``_lock``, so no new batch can be submitted).  This waits on the DEVICE, not
+        on the batches' collection: a leader thread may hold a submitted batch it
+        will only collect after its next submission, which needs ``_lock``."""
+        import torch
+
+        torch.cuda.synchronize(self.engine.device)
 
     def _run_implicit(self, hist, cand, ids: bool):
         """Reference ImplicitShapeRunner (orchestrator.py:225-260): exact-shape
@@ -519,6 +522,14 @@ class DeviceService:
         ids = np.asarray(item_ids, dtype=np.int64).reshape(-1)
         values = list(values)
         d = self.config.hidden_dim
+        if self.feature_cache is not None:
+            # behind the feature cache a pushed value is a cache fill (cache.py:321-325
+            # put): the row is written when a lookup next resolves the key
+            for i, v in zip(ids.tolist(), values):
+                self.feature_cache.put(i, bytes(v))
+            with self._stats_lock:
+                self.feature_bytes += sum(len(v) for v in values)
+            return
         with self._lock:
             self._quiesce()
             self.engine.update_values(ids, values)

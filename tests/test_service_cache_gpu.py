@@ -93,3 +93,61 @@ def test_lru_eviction_reads_as_empty(gpu):
         assert svc.metrics_snapshot()["cache"]["misses"] == 3
     finally:
         svc.close()
+
+
+def test_concurrent_callers_with_async_refreshes(gpu):
+    # 8 threads scoring while background refreshes land: no request fails, every
+    # score is finite, and once the refreshes have drained the same requests score
+    # exactly what a resident (always-fresh) table scores
+    import threading
+
+    svc = DeviceService(CFG, num_items=NUM_ITEMS, target_rows=256, precision="fp32",
+                        cache=CacheConfig(mode=CacheMode.ASYNC, ttl_s=1e9))
+    ref = DeviceService(CFG, num_items=NUM_ITEMS, target_rows=256, precision="fp32")
+    rng = np.random.default_rng(3)
+    reqs = [request_of(rng.integers(0, NUM_ITEMS, 2 * int(rng.integers(0, 33))),
+                       rng.integers(0, NUM_ITEMS, int(rng.integers(1, 33)))) for _ in range(64)]
+    errors = []
+
+    def worker(k):
+        try:
+            for req in reqs[k::8]:
+                out = svc.handle_request(req).scores
+                assert np.isfinite(out).all()
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    try:
+        threads = [threading.Thread(target=worker, args=(k,)) for k in range(8)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        assert not errors, errors[0]
+        svc.feature_cache.drain_refreshes()
+        for req in reqs:
+            svc.handle_request(req)  # lookups after the drain: every key fresh, rows written
+        for req in reqs:
+            np.testing.assert_allclose(svc.handle_request(req).scores, ref.handle_request(req).scores,
+                                       rtol=0, atol=1e-6)
+    finally:
+        svc.close()
+        ref.close()
+
+
+def test_pushed_values_fill_the_cache(gpu):
+    # refresh_values behind the cache is a cache fill (reference FeatureCache.put):
+    # the next lookup of the key is a fresh hit on the pushed value
+    svc = service(CacheMode.SYNC)
+    try:
+        req = request_of(range(4), [50, 51])
+        base = svc.handle_request(req).scores
+        new = rows([51], {51: 3})[0]
+        svc.refresh_values([51], [new.astype("<f8").tobytes() + b"\0" * 64])
+        got = svc.handle_request(req).scores
+        want = orc.model_forward(rows(range(4)), np.stack([rows([50])[0], new]), svc.params, CFG)
+        assert np.abs(got - want).max() <= TOL
+        assert np.abs(got[1] - base[1]).max() > 1e-6
+        assert svc.metrics_snapshot()["cache"]["misses"] == 6  # the pushed key was not fetched
+    finally:
+        svc.close()

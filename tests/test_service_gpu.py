@@ -152,3 +152,46 @@ def test_bf16_table_refresh(gpu):
     want = orc.model_forward(resolve(req.history_item_ids), cand, svc.params, CFG)
     assert np.abs(after - want).max() <= 2e-2
     svc.close()
+
+
+@pytest.mark.timeout(180)
+def test_mutate_while_callers_are_scoring(gpu):
+    # a row refresh waits for the DEVICE (not for the in-flight batches'
+    # collection, which the submitting leader does only after its next submit):
+    # concurrent mutate + scoring must neither deadlock nor fail
+    import threading
+
+    svc = DeviceService(CFG, num_items=NUM_ITEMS, target_rows=256)
+    rng = np.random.default_rng(8)
+    reqs = [request_of(rng.integers(0, NUM_ITEMS, 2 * int(rng.integers(0, 33))),
+                       rng.integers(0, NUM_ITEMS, int(rng.integers(1, 33)))) for _ in range(96)]
+    errors = []
+    stop = threading.Event()
+
+    def caller(k):
+        try:
+            for req in reqs[k::6]:
+                assert np.isfinite(svc.handle_request(req).scores).all()
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    def mutator():
+        i = 0
+        while not stop.is_set():
+            svc.mutate([i % NUM_ITEMS])
+            i += 7
+
+    try:
+        m = threading.Thread(target=mutator)
+        m.start()
+        threads = [threading.Thread(target=caller, args=(k,)) for k in range(6)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        stop.set()
+        m.join()
+        assert not errors, errors[0]
+    finally:
+        stop.set()
+        svc.close()
