@@ -1,7 +1,7 @@
 #!/bin/bash
 # round-2 measurement: bench lines (cfg3 with fp32 line, cfg4, cfg2, cfg5, cfg1), sustained cfg3,
 # reference arm, ncu launch list + full capture of the bench's own cfg3 pass
-O=gpurun_out/m2; mkdir -p $O
+O=gpurun_out/${MEASURE_OUT:-m2}; mkdir -p $O
 for w in cfg3 cfg4 cfg2 cfg5 cfg1; do
   timeout 900 python bench.py --workload $w --steps 20 --warmup 5 > $O/bench_$w.log 2>&1
   tail -1 $O/bench_$w.log > $O/bench_$w.json
@@ -19,3 +19,5 @@ python -c "
 import json; d=json.load(open('$O/bench_cfg3_sustained.json')); print('sustained', d['value'], d['clocks'], d['e2e']['value'])"
 head -c 400 $O/ref_cfg3.json
 tail -2 $O/ncu_full.log
+timeout 600 python tools/serve_bench.py --workload cfg3 --gpus 1 --requests 8000 --window 128 --frame 64 > $O/serve_cfg3.log 2>&1
+tail -1 $O/serve_cfg3.log | cut -c1-300
