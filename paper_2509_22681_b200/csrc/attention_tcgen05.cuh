@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     const uint32_t tS = tmem + i * 256, tP = tS + 128, tO = tS + 192;
     constexpr uint32_t idesc_s = ptx::make_idesc_bf16(kRows, kKeys, 0, 0);
     constexpr uint32_t idesc_o = ptx::make_idesc_bf16(kRows, DH, 0, 1);
-    uint32_t kv_loads[2] = {0, 0}, kv_frees[2] = {0, 0};
+    uint32_t k_loads[2] = {0, 0}, v_loads[2] = {0, 0}, v_frees[2] = {0, 0};
     int res_unit = -1;    // unit whose K/V is resident in the slots (hb <= 256)
     int res_loaded = 0;   // chunks of res_unit already loaded
     auto load_qs = [&](const Job& j) {
@@ -201,20 +201,34 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
       }
       __syncwarp();
     };
-    auto load_kv = [&](const Job& j, int chunk, int slot) {
-      if (kv_loads[slot] > kv_frees[slot]) {  // slot still read by earlier MMAs
-        ptx::mbar_wait(B(i, 6 + slot), kv_frees[slot] & 1);
-        ++kv_frees[slot];
+    // V slot: reusable once the PV that read it completed (kv_free commit)
+    auto load_v = [&](const Job& j, int chunk, int slot) {
+      if (v_loads[slot] > v_frees[slot]) {  // slot still read by an earlier PV
+        ptx::mbar_wait(B(i, 6 + slot), v_frees[slot] & 1);
+        ++v_frees[slot];
       }
       const int row = j.hist_row0 + chunk * kKeys;
       if (leader) {
-        ptx::mbar_arrive_expect_tx(B(i, 2 + slot), kTile);
-        ptx::tma_load_3d(sK + slot * kTile, &tm_qkv, B(i, 2 + slot), a.DA + j.h * DH, row, j.g);
         ptx::mbar_arrive_expect_tx(B(i, 4 + slot), kTile);
         ptx::tma_load_3d(sV + slot * kTile, &tm_qkv, B(i, 4 + slot), 2 * a.DA + j.h * DH, row, j.g);
       }
       __syncwarp();
-      ++kv_loads[slot];
+      ++v_loads[slot];
+    };
+    // K slot: the caller guarantees the S MMA that read it completed
+    auto load_k = [&](const Job& j, int chunk, int slot) {
+      const int row = j.hist_row0 + chunk * kKeys;
+      if (leader) {
+        ptx::mbar_arrive_expect_tx(B(i, 2 + slot), kTile);
+        ptx::tma_load_3d(sK + slot * kTile, &tm_qkv, B(i, 2 + slot), a.DA + j.h * DH, row, j.g);
+      }
+      __syncwarp();
+      ++k_loads[slot];
+    };
+    // both: the V wait (PV done) also orders the K reload after every earlier S on the slot
+    auto load_kv = [&](const Job& j, int chunk, int slot) {
+      load_v(j, chunk, slot);
+      load_k(j, chunk, slot);
     };
     // K/V needed at the start of a job
     auto prepare_kv = [&](const Job& j) {
@@ -246,7 +260,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
     };
     auto issue_s = [&](const Job& jb, int c) {  // S = Q K_c^T into the WG's S columns
       const int slot = jb.nk_all <= 2 ? c : (c & 1);
-      ptx::mbar_wait(B(i, 2 + slot), (kv_loads[slot] - 1) & 1);
+      ptx::mbar_wait(B(i, 2 + slot), (k_loads[slot] - 1) & 1);
       ptx::tc_fence_after();
       const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK + slot * kTile);
       if (leader) {
@@ -310,9 +324,16 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           issue_s(cur, c + 1);
           if (c + 1 == cur.nk - 1) prefetch_next_q();
         }
+        if (!resident) {
+          // streamed chunks, K and V on their own schedules: K_{c+2} takes K_c's slot
+          // (S_c completed: the WG read it), V_{c+1} takes V_{c-1}'s (PV_{c-1} was
+          // issued an iteration ago), each a full chunk ahead of its MMA
+          if (c + 2 < cur.nk) load_k(cur, c + 2, c & 1);
+          if (c >= 1 && c + 1 < cur.nk) load_v(cur, c + 1, (c + 1) & 1);
+        }
         ptx::mbar_wait(B(i, 9), cc & 1);  // WG stored P_c (and rescaled O)
         ATTN_TRACE(2 + i, 14);
-        ptx::mbar_wait(B(i, 4 + slot), (kv_loads[slot] - 1) & 1);
+        ptx::mbar_wait(B(i, 4 + slot), (v_loads[slot] - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t aV = ptx::smem_u32(sV + slot * kTile);
         if (leader) {
@@ -325,9 +346,8 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
         __syncwarp();
         ATTN_TRACE(2 + i, 15);
         if (!resident) {
-          if (leader) ptx::mma_commit(B(i, 6 + slot));
+          if (leader) ptx::mma_commit(B(i, 6 + slot));  // V_c's slot is free once PV_c completes
           __syncwarp();
-          if (c + 2 < cur.nk) load_kv(cur, c + 2, slot);
         } else if (!(nxt.valid && nxt.u == cur.u)) {
           // last job of this unit: recycle slot c as soon as PV_c is issued and,
           // when the next unit is resident too, start loading its chunk c into it
@@ -341,8 +361,8 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
           if (c == cur.nk - 1) {
             // chunks this (causal) tile never used: their TMA must land before reuse
             for (int s = cur.nk; s < cur.nk_all; ++s) {
-              ptx::mbar_wait(B(i, 2 + s), (kv_loads[s] - 1) & 1);
-              ptx::mbar_wait(B(i, 4 + s), (kv_loads[s] - 1) & 1);
+              ptx::mbar_wait(B(i, 2 + s), (k_loads[s] - 1) & 1);
+              ptx::mbar_wait(B(i, 4 + s), (v_loads[s] - 1) & 1);
               if (leader) ptx::mma_commit(B(i, 6 + s));
               __syncwarp();
             }
