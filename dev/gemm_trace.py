@@ -24,7 +24,7 @@ lib.flame_debug_gemm_trace(ctypes.c_void_p(buf.data_ptr()), which)
 ex.run(_lib.INPUT_IDS, graph=False); ex.stream.synchronize()
 lib.flame_debug_gemm_trace(None, -1)
 t = buf.cpu().numpy().astype(np.uint64).reshape(4, 4096)
-names = {1: "M:acc_free", 2: "M:data", 3: "M:commit", 4: "E:full", 5: "E:chunk", 6: "E:free", 7: "P:stage", 8: "E:resid", 9: "E:staged"}
+names = {1: "M:acc_free", 2: "M:data", 3: "M:commit", 4: "E:full", 5: "E:chunk", 6: "E:free", 7: "P:stage", 8: "E:resid", 9: "E:staged", 10: "M:kb_data", 11: "M:kb_wait"}
 t0 = min(int(x >> 8) for row in t for x in row if x)
 for slot in range(4):
     ev = [(int(x >> 8) - t0, int(x & 0xff)) for x in t[slot] if x]

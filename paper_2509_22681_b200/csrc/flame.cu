@@ -1466,6 +1466,34 @@ extern "C" int flame_debug_gemm_trace(void* dev_buf, int which) {
   return 0;
 }
 
+// Debug-only: one tcgen05 GEMM on caller-owned device buffers (dev A/B timing of
+// epilogue variants).  A [G][M][K], W [G][N][K] bf16; out [G][M][N] (bf16, or fp32
+// with EPI_OUT_F32; the gated sum is one [M][N] fp32); resid_b [G][M][N] bf16;
+// bias / gate_w / gate_b [G][N] fp32.
+extern "C" int flame_debug_gemm(int epi, const void* A, const void* W, void* out, const float* bias,
+                                const void* resid_b, const float* gate_w, const float* gate_b, int M, int N,
+                                int K, int G, void* stream, const float* lnstats, const float* colsum,
+                                int stats_parts) {
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  flame::GemmProblem p{};
+  p.A = A; p.lda = K; p.a_gstride = static_cast<long long>(M) * K;
+  p.W = W; p.ldw = K; p.w_gstride = static_cast<long long>(N) * K;
+  p.M = M; p.N = N; p.K = K; p.G = G; p.epi = epi;
+  p.ep.out = out; p.ep.out_ld = N; p.ep.out_gstride = (epi & flame::EPI_GATED) ? 0 : static_cast<long long>(M) * N;
+  p.ep.bias = bias; p.ep.bias_gstride = N;
+  p.ep.resid_b = static_cast<const __nv_bfloat16*>(resid_b); p.ep.resid_ld = N;
+  p.ep.resid_gstride = static_cast<long long>(M) * N;
+  p.ep.gate_w = gate_w; p.ep.gate_b = gate_b;
+  p.ep.lnstats = lnstats; p.ep.lnstats_gstride = static_cast<long long>(M) * stats_parts * 2;
+  p.ep.stats_parts = stats_parts; p.ep.d_true = K;
+  p.ep.colsum = colsum; p.ep.colsum_gstride = N;
+  p.ep.M = M; p.ep.N = N;
+  CUDA_TRY(flame::launch_gemm(p, static_cast<cudaStream_t>(stream), sms));
+  return 0;
+}
+
 extern "C" int flame_debug_attn_trace(void* dev_buf) {
   unsigned long long* p = static_cast<unsigned long long*>(dev_buf);
   CUDA_TRY(cudaMemcpyToSymbol(flame::g_attn_trace, &p, sizeof(p)));

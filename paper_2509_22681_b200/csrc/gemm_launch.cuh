@@ -68,18 +68,18 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   const int m_tiles = (p.M + gemm::BM - 1) / gemm::BM;
   const int n_tiles = (p.N + BN - 1) / BN;
   // CTA pairs halve each CTA's W-tile traffic from L2, which is what paces the
-  // light-epilogue K = 512 GEMMs (measured at cfg3: QKV 0.367 -> 0.323 ms, K/V of
-  // the history 0.136 -> 0.120 ms), and, since the residual loader decodes once
-  // per tile, also O-proj + LN2 statistics (0.175 -> 0.165 ms) and the tf32
-  // expert (0.131 -> 0.120 ms).  The bf16 GELU epilogue (FFN W1) is the limit of
-  // its GEMM instead and loses to the pair handshake below K = 1024
-  // (W1 0.567 -> 0.60 ms), as do all GEMMs with K < 512.
+  // K = 512 GEMMs (measured at cfg3: QKV 0.367 -> 0.323 ms, K/V of the history
+  // 0.136 -> 0.120 ms), and, since the residual loader decodes once per tile, also
+  // O-proj + LN2 statistics (0.175 -> 0.165 ms) and the tf32 expert (0.131 ->
+  // 0.120 ms).  FFN W1 (bf16 GELU epilogue) gains too since the epilogue moved to
+  // fp32 pairs: 0.513 -> 0.459 ms for bias + GELU alone (dev/gemm_ab.py, cfg3
+  // shape), 0.504 -> 0.500 ms in the step, where the folded-LN epilogue is its
+  // limit.  GEMMs with K < 512 keep single CTAs.
   static const int pair_min_k_env = [] {  // FLAME_GEMM_PAIR_MINK overrides (A/B)
     const char* e = getenv("FLAME_GEMM_PAIR_MINK");
     return e ? atoi(e) : 0;
   }();
-  constexpr bool kGeluBf16 = (EPI & EPI_GELU) != 0 && (EPI & (EPI_OUT_F32 | EPI_ROWDOT)) == 0;
-  const int pair_min_k = pair_min_k_env > 0 ? pair_min_k_env : (kGeluBf16 ? 1024 : 512);
+  const int pair_min_k = pair_min_k_env > 0 ? pair_min_k_env : 512;
   const int ncl = (gemm_cluster_pref() == 2 && m_tiles >= 2 && max_clusters > 0 && p.K >= pair_min_k) ? 2 : 1;
   CUtensorMap ta, tb;
   const int ga = p.a_shared ? 1 : p.G;

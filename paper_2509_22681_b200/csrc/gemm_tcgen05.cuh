@@ -349,8 +349,15 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       ptx::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < num_k_blocks; ++kb) {
+#ifdef FLAME_DEBUG_TRACE_KB
+        GEMM_TRACE(0, 11);
+#endif
         ptx::mbar_wait(&full[stage], phase);
+#ifdef FLAME_DEBUG_TRACE_KB
+        GEMM_TRACE(0, 10);
+#else
         if (kb == 0) GEMM_TRACE(0, 2);
+#endif
         ptx::tc_fence_after();
         const uint32_t a_addr = ptx::smem_u32(smem_a + stage * C::kABytes);
         const uint32_t b_addr = ptx::smem_u32(smem_b + stage * C::kBBytes);
