@@ -67,7 +67,14 @@ namespace fattn {
 constexpr int kRows = 128;
 constexpr int kKeys = 128;
 constexpr int DH = 64;
-constexpr int kThreads = 352;
+// 12 warps.  setmaxnreg moves registers from warpgroup 2 (producer, MMA, K/V
+// loader, one idle warp) to the two softmax warpgroups: 2 x 224 + 56 = 504 =
+// 3 x 168, the CTA's launch allocation (the pool setmaxnreg.inc draws from; a
+// larger sum blocks forever).  Measured at cfg3: 0.609 -> 0.596 ms, the spills
+// of the 168-register build (108 bytes) gone.
+constexpr int kThreads = 384;
+constexpr int kRegsSoftmax = 224, kRegsOther = 56;
+static_assert(2 * kRegsSoftmax + kRegsOther <= 3 * 168, "setmaxnreg budget above the launch allocation");
 constexpr int kTile = kRows * DH * 2;           // 16 KB: 128 rows x 64 bf16
 constexpr int kKB = 32;                         // projection k-block depth (64-byte rows)
 constexpr int kATile = kRows * kKB * 2;         // 8 KB: 128 rows x 32 bf16
@@ -153,166 +160,170 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
   };
   const int cand_row0 = a.R * a.hb_bkt;  // first candidate row of the QKV / AO row space
 
-  if (warp == 8) {
-    // ------------------------------------------------ A / W ring producer
-    const bool leader = ptx::elect_one();
-    uint32_t rk = 0;
-    unsigned trace_k = 0;
-    for (int k = 0;; ++k) {
-      const Unit un = unit_at(k);
-      if (!un.valid) break;
-      for (int p = 0; p < un.n_pairs; ++p) {
-        const int t0 = 2 * p;
-        const bool has1 = t0 + 1 < un.n_tiles;
-        const int arow = un.r * a.c_bkt + t0 * kRows;
-        for (int kb = 0; kb < KB; ++kb, ++rk) {
-          const int s = rk % kStages;
-          if (rk >= kStages) ptx::mbar_wait(bars + RING_EMPTY + s, ((rk / kStages) - 1) & 1);
-          ATTN_TRACE(3, 21);
-          if (leader) {
-            uint8_t* st = smem + s * kStageBytes;
-            uint64_t* fb = bars + RING_FULL + s;
-            ptx::mbar_arrive_expect_tx(fb, (has1 ? 2 : 1) * kATile + kWBytes);
-            ptx::tma_load_3d(st, &tm_a, fb, kb * kKB, arow, 0);
-            if (has1) ptx::tma_load_3d(st + kATile, &tm_a, fb, kb * kKB, arow + kRows, 0);
-            uint8_t* w = st + 2 * kATile;
-            ptx::tma_load_3d(w, &tm_w, fb, kb * kKB, un.h * DH, un.g);
-            ptx::tma_load_3d(w + kWPart, &tm_w, fb, kb * kKB, a.DA + un.h * DH, un.g);
-            ptx::tma_load_3d(w + 2 * kWPart, &tm_w, fb, kb * kKB, 2 * a.DA + un.h * DH, un.g);
-          }
-          __syncwarp();
-        }
-      }
-    }
-  } else if (warp == 10) {
-    // ---------------------------------------------- history K / V producer
-    const bool leader = ptx::elect_one();
-    uint32_t ku = 0;
-    for (int k = 0;; ++k) {
-      const Unit un = unit_at(k);
-      if (!un.valid) break;
-      if (un.nk == 0 || un.n_pairs == 0) continue;
-      if (ku > 0) ptx::mbar_wait(bars + KV_FREE, (ku - 1) & 1);  // previous unit's last PV done
-      if (leader) {
-        for (int c = 0; c < un.nk; ++c) {
-          uint64_t* fb = bars + KV_FULL + c;
-          const int row = un.r * a.hb_bkt + c * kKeys;
-          ptx::mbar_arrive_expect_tx(fb, 2 * kTile);
-          ptx::tma_load_3d(smem + kKOff + c * kTile, &tm_qkv, fb, a.DA + un.h * DH, row, un.g);
-          ptx::tma_load_3d(smem + kVOff + c * kTile, &tm_qkv, fb, 2 * a.DA + un.h * DH, row, un.g);
-        }
-      }
-      __syncwarp();
-      ++ku;
-    }
-  } else if (warp == 9) {
-    // ------------------------------------------------------ MMA issuer
-    const bool leader = ptx::elect_one();
-    constexpr uint32_t idesc_p = ptx::make_idesc_bf16(kRows, 3 * DH, 0, 0);
-    constexpr uint32_t idesc_s = ptx::make_idesc_bf16(kRows, kKeys, 0, 0);
-    constexpr uint32_t idesc_o = ptx::make_idesc_bf16(kRows, DH, 0, 1);
-    uint32_t rk = 0, ku = 0;
-    uint32_t nj[2] = {0, 0}, cc[2] = {0, 0};
-    unsigned trace_k = 0;
-    for (int k = 0;; ++k) {
-      const Unit un = unit_at(k);
-      if (!un.valid) break;
-      const bool kv = un.nk > 0 && un.n_pairs > 0;
-      for (int p = 0; p < un.n_pairs; ++p) {
-        const bool has1 = 2 * p + 1 < un.n_tiles;
-        const int nw = has1 ? 2 : 1;
-        // projection: proj_i = A_ti (128 x D) . W_{g,h}^T (D x 192) for both tiles
-        for (int kb = 0; kb < KB; ++kb, ++rk) {
-          const int s = rk % kStages;
-          ptx::mbar_wait(bars + RING_FULL + s, (rk / kStages) & 1);
-          ATTN_TRACE(2, 31);
-          ptx::tc_fence_after();
-          if (leader) {
-            const uint32_t st = ptx::smem_u32(smem + s * kStageBytes);
-            const uint32_t aw = st + 2 * kATile;
-#pragma unroll
-            for (int kk = 0; kk < kKB / 16; ++kk) {
-              const uint64_t bd = ptx::make_desc_sw64(aw + kk * 32, 512);
-              ptx::mma_bf16_ss(tmem, ptx::make_desc_sw64(st + kk * 32, 512), bd, idesc_p, (kb | kk) != 0);
-              if (has1)
-                ptx::mma_bf16_ss(tmem + 256, ptx::make_desc_sw64(st + kATile + kk * 32, 512), bd, idesc_p,
-                                 (kb | kk) != 0);
+  if (warp >= 8) {
+    ptx::setmaxnreg_dec<kRegsOther>();
+    if (warp == 8) {
+      // ------------------------------------------------ A / W ring producer
+      const bool leader = ptx::elect_one();
+      uint32_t rk = 0;
+      unsigned trace_k = 0;
+      for (int k = 0;; ++k) {
+        const Unit un = unit_at(k);
+        if (!un.valid) break;
+        for (int p = 0; p < un.n_pairs; ++p) {
+          const int t0 = 2 * p;
+          const bool has1 = t0 + 1 < un.n_tiles;
+          const int arow = un.r * a.c_bkt + t0 * kRows;
+          for (int kb = 0; kb < KB; ++kb, ++rk) {
+            const int s = rk % kStages;
+            if (rk >= kStages) ptx::mbar_wait(bars + RING_EMPTY + s, ((rk / kStages) - 1) & 1);
+            ATTN_TRACE(3, 21);
+            if (leader) {
+              uint8_t* st = smem + s * kStageBytes;
+              uint64_t* fb = bars + RING_FULL + s;
+              ptx::mbar_arrive_expect_tx(fb, (has1 ? 2 : 1) * kATile + kWBytes);
+              ptx::tma_load_3d(st, &tm_a, fb, kb * kKB, arow, 0);
+              if (has1) ptx::tma_load_3d(st + kATile, &tm_a, fb, kb * kKB, arow + kRows, 0);
+              uint8_t* w = st + 2 * kATile;
+              ptx::tma_load_3d(w, &tm_w, fb, kb * kKB, un.h * DH, un.g);
+              ptx::tma_load_3d(w + kWPart, &tm_w, fb, kb * kKB, a.DA + un.h * DH, un.g);
+              ptx::tma_load_3d(w + 2 * kWPart, &tm_w, fb, kb * kKB, 2 * a.DA + un.h * DH, un.g);
             }
-            ptx::mma_commit(bars + RING_EMPTY + s);
+            __syncwarp();
           }
-          __syncwarp();
         }
+      }
+    } else if (warp == 10) {
+      // ---------------------------------------------- history K / V producer
+      const bool leader = ptx::elect_one();
+      uint32_t ku = 0;
+      for (int k = 0;; ++k) {
+        const Unit un = unit_at(k);
+        if (!un.valid) break;
+        if (un.nk == 0 || un.n_pairs == 0) continue;
+        if (ku > 0) ptx::mbar_wait(bars + KV_FREE, (ku - 1) & 1);  // previous unit's last PV done
         if (leader) {
-          ptx::mma_commit(WB(0, PROJ_FULL));
-          if (has1) ptx::mma_commit(WB(1, PROJ_FULL));
-        }
-        __syncwarp();
-        // each warpgroup stored its Q (bf16) into TMEM: its first S MMA starts at once
-        ATTN_TRACE(2, 32);
-        auto issue_s = [&](int i, int c) {
-          if (p == 0) ptx::mbar_wait(bars + KV_FULL + c, ku & 1);  // first use of chunk c in this unit
-          ptx::tc_fence_after();
-          const uint32_t aK = ptx::smem_u32(smem + kKOff + c * kTile);
-          const uint32_t tS = tmem + i * 256, tQ = tS + 192;
-          if (leader) {
-#pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk)
-              ptx::mma_bf16_ts(tS, tQ + kk * 8, ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
-            ptx::mma_commit(WB(i, S_FULL));
-          }
-          __syncwarp();
-        };
-        for (int i = 0; i < nw; ++i) {
-          ptx::mbar_wait(WB(i, Q_READY), nj[i] & 1);
-          if (un.nk > 0) issue_s(i, 0);
-        }
-        ATTN_TRACE(2, 33);
-        if (un.nk > 0) {
           for (int c = 0; c < un.nk; ++c) {
-            for (int i = 0; i < nw; ++i) {
-              ptx::mbar_wait(WB(i, S_FREE), cc[i] & 1);  // S_c in the WG's registers
-              if (c + 1 < un.nk) {
-                // S_{c+1} runs under the softmax of chunk c (waits for chunk c+1's K only on first use)
-                if (p == 0) ptx::mbar_wait(bars + KV_FULL + c + 1, ku & 1);
-                ptx::tc_fence_after();
-                const uint32_t aK = ptx::smem_u32(smem + kKOff + (c + 1) * kTile);
-                const uint32_t tS = tmem + i * 256, tQ = tS + 192;
-                if (leader) {
-#pragma unroll
-                  for (int kk = 0; kk < DH / 16; ++kk)
-                    ptx::mma_bf16_ts(tS, tQ + kk * 8, ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
-                  ptx::mma_commit(WB(i, S_FULL));
-                }
-                __syncwarp();
-              }
-            }
-            for (int i = 0; i < nw; ++i) {
-              ptx::mbar_wait(WB(i, P_FULL), cc[i] & 1);  // P_c stored (and O rescaled)
-              ATTN_TRACE(2, 35);
-              ptx::tc_fence_after();
-              const uint32_t aV = ptx::smem_u32(smem + kVOff + c * kTile);
-              const uint32_t tP = tmem + i * 256 + 128, tO = tmem + i * 256 + 192;
-              if (leader) {
-#pragma unroll
-                for (int kk = 0; kk < kKeys / 16; ++kk)
-                  ptx::mma_bf16_ts(tO, tP + kk * 8, ptx::make_desc_sw128(aV + kk * 16 * 128, kRows * 128, 1024),
-                                   idesc_o, (c | kk) != 0);
-                ptx::mma_commit(WB(i, O_FULL));
-              }
-              __syncwarp();
-              ++cc[i];
-            }
+            uint64_t* fb = bars + KV_FULL + c;
+            const int row = un.r * a.hb_bkt + c * kKeys;
+            ptx::mbar_arrive_expect_tx(fb, 2 * kTile);
+            ptx::tma_load_3d(smem + kKOff + c * kTile, &tm_qkv, fb, a.DA + un.h * DH, row, un.g);
+            ptx::tma_load_3d(smem + kVOff + c * kTile, &tm_qkv, fb, 2 * a.DA + un.h * DH, row, un.g);
           }
         }
-        for (int i = 0; i < nw; ++i) ++nj[i];
-      }
-      if (kv) {
-        if (leader) ptx::mma_commit(bars + KV_FREE);  // the unit's last PV done -> K / V slots free
         __syncwarp();
         ++ku;
       }
+    } else if (warp == 9) {
+      // ------------------------------------------------------ MMA issuer
+      const bool leader = ptx::elect_one();
+      constexpr uint32_t idesc_p = ptx::make_idesc_bf16(kRows, 3 * DH, 0, 0);
+      constexpr uint32_t idesc_s = ptx::make_idesc_bf16(kRows, kKeys, 0, 0);
+      constexpr uint32_t idesc_o = ptx::make_idesc_bf16(kRows, DH, 0, 1);
+      uint32_t rk = 0, ku = 0;
+      uint32_t nj[2] = {0, 0}, cc[2] = {0, 0};
+      unsigned trace_k = 0;
+      for (int k = 0;; ++k) {
+        const Unit un = unit_at(k);
+        if (!un.valid) break;
+        const bool kv = un.nk > 0 && un.n_pairs > 0;
+        for (int p = 0; p < un.n_pairs; ++p) {
+          const bool has1 = 2 * p + 1 < un.n_tiles;
+          const int nw = has1 ? 2 : 1;
+          // projection: proj_i = A_ti (128 x D) . W_{g,h}^T (D x 192) for both tiles
+          for (int kb = 0; kb < KB; ++kb, ++rk) {
+            const int s = rk % kStages;
+            ptx::mbar_wait(bars + RING_FULL + s, (rk / kStages) & 1);
+            ATTN_TRACE(2, 31);
+            ptx::tc_fence_after();
+            if (leader) {
+              const uint32_t st = ptx::smem_u32(smem + s * kStageBytes);
+              const uint32_t aw = st + 2 * kATile;
+#pragma unroll
+              for (int kk = 0; kk < kKB / 16; ++kk) {
+                const uint64_t bd = ptx::make_desc_sw64(aw + kk * 32, 512);
+                ptx::mma_bf16_ss(tmem, ptx::make_desc_sw64(st + kk * 32, 512), bd, idesc_p, (kb | kk) != 0);
+                if (has1)
+                  ptx::mma_bf16_ss(tmem + 256, ptx::make_desc_sw64(st + kATile + kk * 32, 512), bd, idesc_p,
+                                   (kb | kk) != 0);
+              }
+              ptx::mma_commit(bars + RING_EMPTY + s);
+            }
+            __syncwarp();
+          }
+          if (leader) {
+            ptx::mma_commit(WB(0, PROJ_FULL));
+            if (has1) ptx::mma_commit(WB(1, PROJ_FULL));
+          }
+          __syncwarp();
+          // each warpgroup stored its Q (bf16) into TMEM: its first S MMA starts at once
+          ATTN_TRACE(2, 32);
+          auto issue_s = [&](int i, int c) {
+            if (p == 0) ptx::mbar_wait(bars + KV_FULL + c, ku & 1);  // first use of chunk c in this unit
+            ptx::tc_fence_after();
+            const uint32_t aK = ptx::smem_u32(smem + kKOff + c * kTile);
+            const uint32_t tS = tmem + i * 256, tQ = tS + 192;
+            if (leader) {
+#pragma unroll
+              for (int kk = 0; kk < DH / 16; ++kk)
+                ptx::mma_bf16_ts(tS, tQ + kk * 8, ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
+              ptx::mma_commit(WB(i, S_FULL));
+            }
+            __syncwarp();
+          };
+          for (int i = 0; i < nw; ++i) {
+            ptx::mbar_wait(WB(i, Q_READY), nj[i] & 1);
+            if (un.nk > 0) issue_s(i, 0);
+          }
+          ATTN_TRACE(2, 33);
+          if (un.nk > 0) {
+            for (int c = 0; c < un.nk; ++c) {
+              for (int i = 0; i < nw; ++i) {
+                ptx::mbar_wait(WB(i, S_FREE), cc[i] & 1);  // S_c in the WG's registers
+                if (c + 1 < un.nk) {
+                  // S_{c+1} runs under the softmax of chunk c (waits for chunk c+1's K only on first use)
+                  if (p == 0) ptx::mbar_wait(bars + KV_FULL + c + 1, ku & 1);
+                  ptx::tc_fence_after();
+                  const uint32_t aK = ptx::smem_u32(smem + kKOff + (c + 1) * kTile);
+                  const uint32_t tS = tmem + i * 256, tQ = tS + 192;
+                  if (leader) {
+#pragma unroll
+                    for (int kk = 0; kk < DH / 16; ++kk)
+                      ptx::mma_bf16_ts(tS, tQ + kk * 8, ptx::make_desc_sw128(aK + kk * 32, 16, 1024), idesc_s, kk != 0);
+                    ptx::mma_commit(WB(i, S_FULL));
+                  }
+                  __syncwarp();
+                }
+              }
+              for (int i = 0; i < nw; ++i) {
+                ptx::mbar_wait(WB(i, P_FULL), cc[i] & 1);  // P_c stored (and O rescaled)
+                ATTN_TRACE(2, 35);
+                ptx::tc_fence_after();
+                const uint32_t aV = ptx::smem_u32(smem + kVOff + c * kTile);
+                const uint32_t tP = tmem + i * 256 + 128, tO = tmem + i * 256 + 192;
+                if (leader) {
+#pragma unroll
+                  for (int kk = 0; kk < kKeys / 16; ++kk)
+                    ptx::mma_bf16_ts(tO, tP + kk * 8, ptx::make_desc_sw128(aV + kk * 16 * 128, kRows * 128, 1024),
+                                     idesc_o, (c | kk) != 0);
+                  ptx::mma_commit(WB(i, O_FULL));
+                }
+                __syncwarp();
+                ++cc[i];
+              }
+            }
+          }
+          for (int i = 0; i < nw; ++i) ++nj[i];
+        }
+        if (kv) {
+          if (leader) ptx::mma_commit(bars + KV_FREE);  // the unit's last PV done -> K / V slots free
+          __syncwarp();
+          ++ku;
+        }
+      }
     }
-  } else if (warp < 8) {
+  } else {
+    ptx::setmaxnreg_inc<kRegsSoftmax>();
     // ---------------------------------- projection epilogue, softmax, output
     const int i = warp >> 2;
     const int row = threadIdx.x & 127;

@@ -23,6 +23,17 @@ __device__ __forceinline__ uint32_t lane_id() {
   return l;
 }
 
+// Per-warpgroup register budget (all four warps of the warpgroup execute it):
+// producer-side warpgroups give registers back, the softmax warpgroups take them
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
