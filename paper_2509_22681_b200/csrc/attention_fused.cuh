@@ -351,7 +351,9 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
         ATTN_TRACE(i, 41);
         ptx::tc_fence_after();
         // ---- projection epilogue: q = rs * acc + c_q (folded LN1), same for k, v
-        float dot = 0.f;
+        // (fp32 pairs: FFMA2 does two lanes' worth per issue slot)
+        const uint64_t rs2 = f2::make(rs, rs);
+        uint64_t dot2 = f2::make(0.f, 0.f);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t qa[32], ka[32];
@@ -363,18 +365,25 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
           for (int e = 0; e < 32; e += 4) {
             const float4 bq = __ldg(reinterpret_cast<const float4*>(cq + half * 32 + e));
             const float4 bk = __ldg(reinterpret_cast<const float4*>(ck + half * 32 + e));
-            const float q0 = fmaf(rs, __uint_as_float(qa[e]), bq.x), q1 = fmaf(rs, __uint_as_float(qa[e + 1]), bq.y);
-            const float q2 = fmaf(rs, __uint_as_float(qa[e + 2]), bq.z), q3 = fmaf(rs, __uint_as_float(qa[e + 3]), bq.w);
-            const float k0 = fmaf(rs, __uint_as_float(ka[e]), bk.x), k1 = fmaf(rs, __uint_as_float(ka[e + 1]), bk.y);
-            const float k2 = fmaf(rs, __uint_as_float(ka[e + 2]), bk.z), k3 = fmaf(rs, __uint_as_float(ka[e + 3]), bk.w);
-            dot = fmaf(q0, k0, dot);
-            dot = fmaf(q1, k1, dot);
-            dot = fmaf(q2, k2, dot);
-            dot = fmaf(q3, k3, dot);
+            const uint64_t q01 = f2::fma(rs2, f2::make(__uint_as_float(qa[e]), __uint_as_float(qa[e + 1])), f2::make(bq.x, bq.y));
+            const uint64_t q23 = f2::fma(rs2, f2::make(__uint_as_float(qa[e + 2]), __uint_as_float(qa[e + 3])), f2::make(bq.z, bq.w));
+            const uint64_t k01 = f2::fma(rs2, f2::make(__uint_as_float(ka[e]), __uint_as_float(ka[e + 1])), f2::make(bk.x, bk.y));
+            const uint64_t k23 = f2::fma(rs2, f2::make(__uint_as_float(ka[e + 2]), __uint_as_float(ka[e + 3])), f2::make(bk.z, bk.w));
+            dot2 = f2::fma(q01, k01, dot2);
+            dot2 = f2::fma(q23, k23, dot2);
+            float q0, q1, q2, q3;
+            f2::split(q01, q0, q1);
+            f2::split(q23, q2, q3);
             qb[e / 2] = pack_bf16x2(q0, q1);
             qb[e / 2 + 1] = pack_bf16x2(q2, q3);
           }
           ptx::tmem_st_32x32b_x16(tQ + half * 16, qb);
+        }
+        float dot;
+        {
+          float d0, d1;
+          f2::split(dot2, d0, d1);
+          dot = d0 + d1;
         }
         // Q is in TMEM: the S MMAs may start (they overwrite q | k, columns [0, 128);
         // v, read below, lives in [128, 192), which only this warpgroup's P
@@ -403,11 +412,16 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
             const int e = c8 * 8;
             const float4 b0 = __ldg(reinterpret_cast<const float4*>(cv + half * 32 + e));
             const float4 b1 = __ldg(reinterpret_cast<const float4*>(cv + half * 32 + e + 4));
+            float v[8];
+            f2::split(f2::fma(rs2, f2::make(__uint_as_float(va[e]), __uint_as_float(va[e + 1])), f2::make(b0.x, b0.y)), v[0], v[1]);
+            f2::split(f2::fma(rs2, f2::make(__uint_as_float(va[e + 2]), __uint_as_float(va[e + 3])), f2::make(b0.z, b0.w)), v[2], v[3]);
+            f2::split(f2::fma(rs2, f2::make(__uint_as_float(va[e + 4]), __uint_as_float(va[e + 5])), f2::make(b1.x, b1.y)), v[4], v[5]);
+            f2::split(f2::fma(rs2, f2::make(__uint_as_float(va[e + 6]), __uint_as_float(va[e + 7])), f2::make(b1.z, b1.w)), v[6], v[7]);
             uint4 w;
-            w.x = pack_bf16x2(fmaf(rs, __uint_as_float(va[e]), b0.x), fmaf(rs, __uint_as_float(va[e + 1]), b0.y));
-            w.y = pack_bf16x2(fmaf(rs, __uint_as_float(va[e + 2]), b0.z), fmaf(rs, __uint_as_float(va[e + 3]), b0.w));
-            w.z = pack_bf16x2(fmaf(rs, __uint_as_float(va[e + 4]), b1.x), fmaf(rs, __uint_as_float(va[e + 5]), b1.y));
-            w.w = pack_bf16x2(fmaf(rs, __uint_as_float(va[e + 6]), b1.z), fmaf(rs, __uint_as_float(va[e + 7]), b1.w));
+            w.x = pack_bf16x2(v[0], v[1]);
+            w.y = pack_bf16x2(v[2], v[3]);
+            w.z = pack_bf16x2(v[4], v[5]);
+            w.w = pack_bf16x2(v[6], v[7]);
             *reinterpret_cast<uint4*>(stage + ptx::sw128_offset(row, (half * 32 + e) * 2)) = w;
           }
         }
@@ -483,8 +497,14 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
               for (int q = 0; q < DH / 32; ++q)
                 ptx::tmem_ld_32x32b_x32(tO + q * 32, *reinterpret_cast<uint32_t(*)[32]>(ov + q * 32));
               ptx::tmem_ld_wait();
+              const uint64_t al2 = f2::make(alpha, alpha);
 #pragma unroll
-              for (int e = 0; e < DH; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+              for (int e = 0; e < DH; e += 2) {
+                float o0, o1;
+                f2::split(f2::mul(f2::make(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])), al2), o0, o1);
+                ov[e] = __float_as_uint(o0);
+                ov[e + 1] = __float_as_uint(o1);
+              }
 #pragma unroll
               for (int q = 0; q < DH / 16; ++q)
                 ptx::tmem_st_32x32b_x16(tO + q * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + q * 16));
@@ -524,20 +544,27 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 v = __bfloat1622float2(v2[e]);
-            o[c8 * 8 + 2 * e] = fmaf(w_self, v.x, o[c8 * 8 + 2 * e]);
-            o[c8 * 8 + 2 * e + 1] = fmaf(w_self, v.y, o[c8 * 8 + 2 * e + 1]);
+            float& oa = o[c8 * 8 + 2 * e];
+            float& ob = o[c8 * 8 + 2 * e + 1];
+            f2::split(f2::fma(f2::make(w_self, w_self), f2::make(v.x, v.y), f2::make(oa, ob)), oa, ob);
           }
         }
-        const float inv = 1.f / l;
+        {
+          // fold 1 / l in here, so the stores below only pack
+          const float inv = 1.f / l;
+          const uint64_t inv2 = f2::make(inv, inv);
+#pragma unroll
+          for (int e = 0; e < DH; e += 2) f2::split(f2::mul(f2::make(o[e], o[e + 1]), inv2), o[e], o[e + 1]);
+        }
         const int q_row0 = cand_row0 + un.r * a.c_bkt + t * kRows;
         if (a.store_tma) {
 #pragma unroll
           for (int c8 = 0; c8 < DH / 8; ++c8) {
             uint4 w;
-            w.x = pack_bf16x2(o[c8 * 8 + 0] * inv, o[c8 * 8 + 1] * inv);
-            w.y = pack_bf16x2(o[c8 * 8 + 2] * inv, o[c8 * 8 + 3] * inv);
-            w.z = pack_bf16x2(o[c8 * 8 + 4] * inv, o[c8 * 8 + 5] * inv);
-            w.w = pack_bf16x2(o[c8 * 8 + 6] * inv, o[c8 * 8 + 7] * inv);
+            w.x = pack_bf16x2(o[c8 * 8 + 0], o[c8 * 8 + 1]);
+            w.y = pack_bf16x2(o[c8 * 8 + 2], o[c8 * 8 + 3]);
+            w.z = pack_bf16x2(o[c8 * 8 + 4], o[c8 * 8 + 5]);
+            w.w = pack_bf16x2(o[c8 * 8 + 6], o[c8 * 8 + 7]);
             *reinterpret_cast<uint4*>(stage + ptx::sw128_offset(row, c8 * 16)) = w;
           }
           ptx::fence_proxy_async_smem();
@@ -554,10 +581,10 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
 #pragma unroll
             for (int c8 = 0; c8 < DH / 8; ++c8) {
               uint4 w;
-              w.x = pack_bf16x2(o[c8 * 8 + 0] * inv, o[c8 * 8 + 1] * inv);
-              w.y = pack_bf16x2(o[c8 * 8 + 2] * inv, o[c8 * 8 + 3] * inv);
-              w.z = pack_bf16x2(o[c8 * 8 + 4] * inv, o[c8 * 8 + 5] * inv);
-              w.w = pack_bf16x2(o[c8 * 8 + 6] * inv, o[c8 * 8 + 7] * inv);
+              w.x = pack_bf16x2(o[c8 * 8 + 0], o[c8 * 8 + 1]);
+              w.y = pack_bf16x2(o[c8 * 8 + 2], o[c8 * 8 + 3]);
+              w.z = pack_bf16x2(o[c8 * 8 + 4], o[c8 * 8 + 5]);
+              w.w = pack_bf16x2(o[c8 * 8 + 6], o[c8 * 8 + 7]);
               reinterpret_cast<uint4*>(dst)[c8] = w;
             }
           }

@@ -81,7 +81,7 @@ constexpr int kSmemBytes = 2 * kWGBytes + 1024 + 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef FLAME_ATTN_POLY_MASK
-#define FLAME_ATTN_POLY_MASK 0xA4  // pairs 2, 5, 7 of every 8 (3/8 of the exponentials)
+#define FLAME_ATTN_POLY_MASK 0x24  // pairs 2 and 5 of every 8 (1/4 of the exponentials)
 #endif
 constexpr unsigned kPolyMask = FLAME_ATTN_POLY_MASK;
 
