@@ -530,8 +530,14 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
             for (int k = 0; k < DH / 32; ++k)
               ptx::tmem_ld_32x32b_x32(tO + k * 32, *reinterpret_cast<uint32_t(*)[32]>(ov + k * 32));
             ptx::tmem_ld_wait();
+            const uint64_t al2 = f2::make(alpha, alpha);
 #pragma unroll
-            for (int e = 0; e < DH; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            for (int e = 0; e < DH; e += 2) {
+              float o0, o1;
+              f2::split(f2::mul(f2::make(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])), al2), o0, o1);
+              ov[e] = __float_as_uint(o0);
+              ov[e + 1] = __float_as_uint(o1);
+            }
 #pragma unroll
             for (int k = 0; k < DH / 16; ++k)
               ptx::tmem_st_32x32b_x16(tO + k * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + k * 16));
@@ -573,22 +579,29 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 v = __bfloat1622float2(v2[e]);
-            o[c * 8 + 2 * e] = fmaf(w_self, v.x, o[c * 8 + 2 * e]);
-            o[c * 8 + 2 * e + 1] = fmaf(w_self, v.y, o[c * 8 + 2 * e + 1]);
+            float& oa = o[c * 8 + 2 * e];
+            float& ob = o[c * 8 + 2 * e + 1];
+            f2::split(f2::fma(f2::make(w_self, w_self), f2::make(v.x, v.y), f2::make(oa, ob)), oa, ob);
           }
         }
       }
-      const float inv = 1.f / l;
+      {
+        // 1 / l folded in here (fp32 pairs), so the stores below only pack
+        const float inv = 1.f / l;
+        const uint64_t inv2 = f2::make(inv, inv);
+#pragma unroll
+        for (int e = 0; e < DH; e += 2) f2::split(f2::mul(f2::make(o[e], o[e + 1]), inv2), o[e], o[e + 1]);
+      }
       if (a.store_tma) {
         // stage the bf16 rows over the V_self tile (each thread rewrites exactly the
         // row it just read); the control warp TMA-stores the 128 x 64 tile
 #pragma unroll
         for (int c = 0; c < DH / 8; ++c) {
           uint4 w;
-          w.x = pack_bf16x2(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
-          w.y = pack_bf16x2(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
-          w.z = pack_bf16x2(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
-          w.w = pack_bf16x2(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
+          w.x = pack_bf16x2(o[c * 8 + 0], o[c * 8 + 1]);
+          w.y = pack_bf16x2(o[c * 8 + 2], o[c * 8 + 3]);
+          w.z = pack_bf16x2(o[c * 8 + 4], o[c * 8 + 5]);
+          w.w = pack_bf16x2(o[c * 8 + 6], o[c * 8 + 7]);
           *reinterpret_cast<uint4*>(stage + ptx::sw128_offset(row, c * 16)) = w;
         }
         ptx::fence_proxy_async_smem();
@@ -597,10 +610,10 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
 #pragma unroll
         for (int c = 0; c < DH / 8; ++c) {
           uint4 w;
-          w.x = pack_bf16x2(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
-          w.y = pack_bf16x2(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
-          w.z = pack_bf16x2(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
-          w.w = pack_bf16x2(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
+          w.x = pack_bf16x2(o[c * 8 + 0], o[c * 8 + 1]);
+          w.y = pack_bf16x2(o[c * 8 + 2], o[c * 8 + 3]);
+          w.z = pack_bf16x2(o[c * 8 + 4], o[c * 8 + 5]);
+          w.w = pack_bf16x2(o[c * 8 + 6], o[c * 8 + 7]);
           reinterpret_cast<uint4*>(dst)[c] = w;
         }
       }
