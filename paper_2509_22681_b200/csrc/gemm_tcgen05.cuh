@@ -179,7 +179,10 @@ struct Cfg {
   static constexpr int kResidBytes = kResidTma ? 2 * kResidBox : 0;
   static constexpr int kFixed = kEpiWarps * (kBoxBytes + kCvecBytes + kResidBytes) + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int kStagesFit = (kSmemBudget - kFixed) / kStageBytes;
-  static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
+#ifndef FLAME_GEMM_MAX_STAGES
+#define FLAME_GEMM_MAX_STAGES 6
+#endif
+  static constexpr int kStages = kStagesFit > FLAME_GEMM_MAX_STAGES ? FLAME_GEMM_MAX_STAGES : kStagesFit;
   static_assert(kStages >= 2, "GEMM smem ring too shallow");
   // two accumulators (+ the gated running sum at columns [2 BN, 3 BN))
   // accumulator ring: as many BN-column buffers as TMEM holds (BN = 128: four), so
