@@ -168,6 +168,7 @@ class MultiDeviceService:
                 self._kill()
                 raise DispatchError(f"worker {rank} failed to start: {msg[1]}")
         self.n = n_devices
+        self._alive = [True] * n_devices  # a worker that exited or died takes no more requests
         self._lock = threading.Lock()
         self._send_locks = [threading.Lock() for _ in range(n_devices)]
         self._outstanding = [0] * n_devices
@@ -197,6 +198,7 @@ class MultiDeviceService:
                 msg = ("died", rank)
             if msg[0] in ("closed", "died"):
                 with self._lock:
+                    self._alive[rank] = False
                     dead = [t for t, (r, _, _, _) in self._pending.items() if r == rank]
                     for tag in dead:
                         _, fut, _, _ = self._pending.pop(tag)
@@ -247,9 +249,12 @@ class MultiDeviceService:
                 from .service import ServiceClosedError
 
                 raise ServiceClosedError("dispatcher is closed")
+            live = [q for q in range(self.n) if self._alive[q]]
+            if not live:
+                raise DispatchError("no live workers")
             for k, (h, c) in enumerate(zip(hs, cs)):
                 work = request_work(h.size, c.size, self.num_blocks)
-                rank = min(range(self.n), key=lambda q: (self._outstanding[q], q))
+                rank = min(live, key=lambda q: (self._outstanding[q], q))
                 self._outstanding[rank] += work
                 self._tag += 1
                 self._pending[self._tag] = (rank, futs[k], work, t0)
@@ -261,8 +266,19 @@ class MultiDeviceService:
             msg = ("frame", tags, np.array([hs[k].size for k in idx], dtype=np.int64),
                    np.array([cs[k].size for k in idx], dtype=np.int64),
                    np.concatenate([hs[k] for k in idx]), np.concatenate([cs[k] for k in idx]))
-            with self._send_locks[rank]:
-                self._conns[rank].send(msg)
+            try:
+                with self._send_locks[rank]:
+                    self._conns[rank].send(msg)
+            except (BrokenPipeError, EOFError, OSError) as exc:
+                # the worker went away between routing and sending: fail its share
+                # now (its reader may already have drained the pending table)
+                with self._lock:
+                    self._alive[rank] = False
+                    lost = [self._pending.pop(int(t)) for t in tags if int(t) in self._pending]
+                    for r, _, work, _ in lost:
+                        self._outstanding[r] -= work
+                for _, fut, _, _ in lost:
+                    fut.set_exception(DispatchError(f"worker {rank} is gone: {exc!r}"))
         return futs
 
     def score(self, requests) -> list:
@@ -312,6 +328,11 @@ class MultiDeviceService:
     def outstanding(self) -> list:
         with self._lock:
             return list(self._outstanding)
+
+    def alive(self) -> list:
+        """Which workers still take requests."""
+        with self._lock:
+            return list(self._alive)
 
     def close(self, timeout_s: float = 60.0) -> None:
         with self._lock:

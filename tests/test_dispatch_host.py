@@ -116,3 +116,26 @@ def test_http_over_the_dispatcher(svc):
     assert client.post("/score", json={"user_id": 1, "history": [1], "candidates": []}).status_code == 400
     m = client.get("/metrics").json()
     assert m["requests_total"] >= 1 and m["workers"] == 2
+
+
+def test_dead_worker_is_routed_around():
+    # a worker that dies fails the requests it held and takes no new ones; the
+    # stream continues on the survivors
+    s = MultiDeviceService(n_devices=2, scorer_factory=StubFactory(), start_timeout_s=120)
+    try:
+        s._procs[0].kill()
+        deadline = time.time() + 60
+        while s.alive()[0] and time.time() < deadline:
+            time.sleep(0.05)
+        assert s.alive() == [False, True]
+        out = s.score([(np.arange(4), np.arange(3)) for _ in range(6)])
+        assert all(int(o[0, 1]) == 1 for o in out)
+        s._procs[1].kill()
+        while s.alive()[1] and time.time() < deadline:
+            time.sleep(0.05)
+        from paper_2509_22681_b200.dispatch import DispatchError
+
+        with pytest.raises(DispatchError):
+            s.submit(np.zeros(2, dtype=np.int64), np.arange(2))
+    finally:
+        s.close(timeout_s=5)
