@@ -379,16 +379,20 @@ class DeviceService:
             self.hits += hits
             self.feature_bytes += nbytes
         order = [i for i, f in enumerate(on_dev) if f] + [i for i, f in enumerate(on_dev) if not f]
-        writes: dict = {}
+        resolved = []
         if self.feature_cache is not None:
-            # reference resolve order: per request, history then candidates (service.py:136-137);
-            # the rows each lookup resolved are written before the batch runs
-            for t, f in zip(batch, on_dev):
-                if f:
-                    w = self.feature_cache.lookup_lists((t.hist, t.cand))
-                    if w is not None:
-                        writes.update(zip(w[0].tolist(), w[1]))
+            # reference resolve order: per request, history then candidates
+            # (service.py:136-137), outside the lock (sync mode may wait on the store)
+            resolved = [self.feature_cache.resolve_lists((t.hist, t.cand)) for t, f in zip(batch, on_dev) if f]
         with self._lock:
+            # the rows each lookup resolved are written before the batch runs; the
+            # write plan is made under the same lock as the writes, so two batches'
+            # plans cannot land on the device in the opposite order
+            writes: dict = {}
+            for seen in resolved:
+                w = self.feature_cache.device_writes(seen)
+                if w is not None:
+                    writes.update(zip(w[0].tolist(), w[1]))
             if writes:
                 self._write_rows(writes)
             if self.routing == "explicit":

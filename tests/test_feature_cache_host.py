@@ -167,3 +167,22 @@ def test_async_batch_reads_empty_until_a_later_lookup():
     ids, rows = cache.lookup_lists([np.array([1, 2])])  # refreshed: fresh hits, rows written now
     assert sorted(ids.tolist()) == [1, 2] and np.abs(rows).sum() > 0
     cache.close()
+
+
+def test_write_plans_follow_the_order_they_are_applied_in():
+    # two batches resolve an id to different values (a refresh landed in between);
+    # whichever plan is applied last is what the row record says, so a later batch
+    # that resolves the other value rewrites the row (the device service makes and
+    # applies the plans under one lock)
+    store = Store(dim=4)
+    cache = make(store, bucket_count=1, capacity_per_bucket=8, ttl_s=100.0, mode=CacheMode.SYNC)
+    seen_a = cache.resolve_lists([np.array([7])])
+    cache.put(7, b"")  # the value changes (EMPTY) before the second batch resolves it
+    seen_b = cache.resolve_lists([np.array([7])])
+    assert seen_b[7] == b"" and seen_a[7] != b""
+    assert cache.device_writes(seen_b) is None  # EMPTY = the zero row already there
+    ids, rows = cache.device_writes(seen_a)  # applied last: the row now holds a's value
+    assert ids.tolist() == [7] and np.abs(rows).sum() > 0
+    ids, rows = cache.device_writes(cache.resolve_lists([np.array([7])]))  # EMPTY again: zero row written
+    assert ids.tolist() == [7] and np.abs(rows).sum() == 0
+    cache.close()
