@@ -81,7 +81,10 @@ constexpr int kATile = kRows * kKB * 2;         // 8 KB: 128 rows x 32 bf16
 constexpr int kWPart = DH * kKB * 2;            // 4 KB: 64 rows of W x 32 bf16
 constexpr int kWBytes = 3 * kWPart;             // 12 KB: q | k | v rows of W, 32 k
 constexpr int kStageBytes = 2 * kATile + kWBytes;  // 28 KB
-constexpr int kStages = 4;
+#ifndef FLAME_FATTN_STAGES
+#define FLAME_FATTN_STAGES 4
+#endif
+constexpr int kStages = FLAME_FATTN_STAGES;
 constexpr int kKOff = kStages * kStageBytes;    // history K chunks [2]
 constexpr int kVOff = kKOff + 2 * kTile;        // history V chunks [2]
 constexpr int kStgOff = kVOff + 2 * kTile;      // per-WG V_self / output staging [2]
@@ -181,13 +184,19 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
             if (leader) {
               uint8_t* st = smem + s * kStageBytes;
               uint64_t* fb = bars + RING_FULL + s;
-              ptx::mbar_arrive_expect_tx(fb, (has1 ? 2 : 1) * kATile + kWBytes);
+#ifdef FLAME_FATTN_DBG_SKIP_W
+              // timing experiment only (wrong results): load FLAME_FATTN_DBG_SKIP_W fewer W parts
+              constexpr int kWLoads = 3 - FLAME_FATTN_DBG_SKIP_W;
+#else
+              constexpr int kWLoads = 3;
+#endif
+              ptx::mbar_arrive_expect_tx(fb, (has1 ? 2 : 1) * kATile + kWLoads * kWPart);
               ptx::tma_load_3d(st, &tm_a, fb, kb * kKB, arow, 0);
               if (has1) ptx::tma_load_3d(st + kATile, &tm_a, fb, kb * kKB, arow + kRows, 0);
               uint8_t* w = st + 2 * kATile;
-              ptx::tma_load_3d(w, &tm_w, fb, kb * kKB, un.h * DH, un.g);
-              ptx::tma_load_3d(w + kWPart, &tm_w, fb, kb * kKB, a.DA + un.h * DH, un.g);
-              ptx::tma_load_3d(w + 2 * kWPart, &tm_w, fb, kb * kKB, 2 * a.DA + un.h * DH, un.g);
+#pragma unroll
+              for (int part = 0; part < kWLoads; ++part)
+                ptx::tma_load_3d(w + part * kWPart, &tm_w, fb, kb * kKB, part * a.DA + un.h * DH, un.g);
             }
             __syncwarp();
           }
