@@ -46,15 +46,17 @@ class DispatchError(RuntimeError):
 
 
 class ServiceFactory:
-    """Default worker scorer: a DeviceService on GPU ``rank`` (picklable for spawn)."""
+    """Default worker scorer: a DeviceService on GPU ``devices[rank]`` (``rank``
+    when no device map is given); picklable for spawn."""
 
-    def __init__(self, config) -> None:
+    def __init__(self, config, devices=None) -> None:
         self.config = config
+        self.devices = list(devices) if devices is not None else None
 
     def __call__(self, rank: int):
         from .service import DeviceService
 
-        return DeviceService.from_config(self.config, device=rank)
+        return DeviceService.from_config(self.config, device=self.devices[rank] if self.devices else rank)
 
 
 def _worker_main(rank: int, conn, factory, max_batch: int, handlers: int) -> None:
@@ -142,13 +144,17 @@ class MultiDeviceService:
     """Front end of N per-GPU workers with least-outstanding-work routing."""
 
     def __init__(self, config=None, n_devices: int = 1, *, scorer_factory=None, max_batch: int = 256,
-                 handlers: int = 2, start_timeout_s: float = 600.0) -> None:
+                 handlers: int = 2, start_timeout_s: float = 600.0, devices=None) -> None:
+        """``devices``: the GPU of each worker (default: worker k on GPU k); two
+        workers may share a GPU (tests on a one-GPU box)."""
         if n_devices < 1:
             raise ValueError("n_devices must be >= 1")
+        if devices is not None and len(devices) != n_devices:
+            raise ValueError("devices must name one GPU per worker")
         if scorer_factory is None:
             if config is None:
                 raise ValueError("a ServiceConfig or a scorer_factory is required")
-            scorer_factory = ServiceFactory(config)
+            scorer_factory = ServiceFactory(config, devices)
         self.num_blocks = config.model.num_blocks if config is not None else 1
         ctx = mp.get_context("spawn")
         self._conns, self._procs = [], []
