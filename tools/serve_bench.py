@@ -36,13 +36,16 @@ def main() -> None:
     ap.add_argument("--window", type=int, default=256)
     ap.add_argument("--warmup", type=int, default=300)
     ap.add_argument("--frame", type=int, default=16, help="requests per submit_many call (one message per worker)")
+    ap.add_argument("--workers-per-gpu", type=int, default=1,
+                    help="worker processes per GPU (the host side of a worker is the limit of one)")
     a = ap.parse_args()
     d, dh, nb, L, f, tasks, H, C, *_ = bench.WORKLOADS[a.workload]
     cfg = ServiceConfig(model=bench.model_config(a.workload), num_items=bench.NUM_ITEMS,
                         store_seed=bench.STORE_SEED, target_rows=64 * 512, max_batch=64)
     reqs = bench.make_requests(a.requests + a.warmup, H, C, bench.WORKLOAD_SEED, a.workload in bench.ZIPF_C)
     t_start = time.perf_counter()
-    with MultiDeviceService(cfg, n_devices=a.gpus) as svc:
+    devices = [g for g in range(a.gpus) for _ in range(a.workers_per_gpu)]
+    with MultiDeviceService(cfg, n_devices=len(devices), devices=devices) as svc:
         startup = time.perf_counter() - t_start
         for fut in svc.submit_many(reqs[: a.warmup]):
             fut.result()
@@ -65,10 +68,10 @@ def main() -> None:
         routed = list(svc.routed)
     lat.sort()
     line = {"metric": "served candidates/s through the process-per-GPU dispatcher", "workload": a.workload,
-            "n_gpus": a.gpus, "requests": a.requests, "window": a.window, "frame": a.frame, "value": cands / wall,
+            "n_gpus": a.gpus, "workers_per_gpu": a.workers_per_gpu, "requests": a.requests, "window": a.window, "frame": a.frame, "value": cands / wall,
             "unit": "candidates/s", "wall_s": wall, "startup_s": startup,
             "p50_ms": 1000 * bench.nearest_rank(lat, 0.5), "p99_ms": 1000 * bench.nearest_rank(lat, 0.99),
-            "routed_per_gpu": routed,
+            "routed_per_worker": routed,
             "latency": "submit (numpy ids, caller process) -> scores back in the caller, per request"}
     print(json.dumps(line), flush=True)
 
