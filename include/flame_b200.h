@@ -137,18 +137,6 @@ int flame_exec_set_staging(FlameExec* ex, const FlameStaging* staging);
  * captured on first use per input mode), copy n_score_rows score rows back, and
  * record the executor's completion event.  Returns without waiting. */
 int flame_exec_submit(FlameExec* ex, int input_mode, int n_req, long long n_score_rows, void* stream);
-/* Id-path submit of a group gathered from a whole batch, in one call (the DSO's
- * per-group host work): request idx[i] (i < n_req) of the batch — ids
- * hist_flat[hist_off[k] .. + hist_len[k]] and cand_flat[cand_off[k] .. +
- * cand_len[k]], k = idx[i] — goes to slot i of the executor's pinned staging; the
- * metadata block is filled, the lengths validated (status 1 with the message of
- * the Python staging checks, nothing staged), n_score_rows set to the group's
- * candidate count, then flame_exec_submit(ex, FLAME_INPUT_IDS, ...).  Replaces
- * the per-request Python packing of orchestrator.py:209-213's executor copies. */
-int flame_exec_submit_ids_gather(FlameExec* ex, const long long* hist_flat, const long long* hist_off,
-                                 const long long* hist_len, const long long* cand_flat, const long long* cand_off,
-                                 const long long* cand_len, const long long* idx, int n_req,
-                                 long long* n_score_rows, void* stream);
 /* Wait for (1) / poll (returns 1 done, 0 pending) the last flame_exec_submit. */
 int flame_exec_wait(FlameExec* ex);
 int flame_exec_query(FlameExec* ex);

@@ -22,7 +22,7 @@ TABLE_BF16, TABLE_FP32 = 0, 1
 EXPORTED = (
     "flame_create", "flame_create_flmp", "flame_destroy", "flame_set_table", "flame_update_table",
     "flame_update_table_values", "flame_pack_padded", "flame_exec_set_staging", "flame_exec_submit",
-    "flame_exec_submit_ids_gather", "flame_exec_wait", "flame_exec_query",
+    "flame_exec_wait", "flame_exec_query",
     "flame_exec_list_capacity", "flame_exec_create", "flame_exec_destroy", "flame_exec_run",
     "flame_exec_capture", "flame_exec_replay", "flame_exec_launch_count", "flame_exec_workspace",
     "flame_exec_profile",
@@ -77,7 +77,6 @@ def load() -> ctypes.CDLL:
             "flame_pack_padded": (I, [P, LL, P, P, LL, LL]),
             "flame_exec_set_staging": (I, [P, ctypes.POINTER(FlameStaging)]),
             "flame_exec_submit": (I, [P, I, I, LL, P]),
-            "flame_exec_submit_ids_gather": (I, [P, P, P, P, P, P, P, P, I, ctypes.POINTER(LL), P]),
             "flame_exec_wait": (I, [P]),
             "flame_exec_query": (I, [P]),
             "flame_exec_list_capacity": (I, [I, I, I]),

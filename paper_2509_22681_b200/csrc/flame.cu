@@ -1372,47 +1372,6 @@ int flame_exec_submit(FlameExec* e, int mode, int n_req, long long n_score_rows,
   return 0;
 }
 
-int flame_exec_submit_ids_gather(FlameExec* e, const long long* hist_flat, const long long* hist_off,
-                                 const long long* hist_len, const long long* cand_flat, const long long* cand_off,
-                                 const long long* cand_len, const long long* idx, int n_req,
-                                 long long* n_score_rows, void* stream) {
-  if (!e || !e->has_stg) return fail(1, "executor has no staging buffers (flame_exec_set_staging)");
-  if (n_req < 0 || n_req > e->R) return fail(1, "batch exceeds executor capacity");
-  if (n_req > 0 && (!hist_off || !hist_len || !cand_flat || !cand_off || !cand_len || !idx || !n_score_rows))
-    return fail(1, "null argument");
-  const FlameStaging& st = e->stg;
-  if (!st.h_hist_ids || !st.h_cand_ids || !st.h_meta) return fail(1, "executor was built without id buffers");
-  const int G = e->ctx->G;
-  // validate first: a rejected group leaves the staging untouched
-  for (int i = 0; i < n_req; ++i) {
-    const long long k = idx[i], h = hist_len[k], c = cand_len[k];
-    if (h % G != 0)
-      return fail(1, "history length " + std::to_string(h) + " is not divisible by num_blocks " + std::to_string(G));
-    if (h > e->H_bkt)
-      return fail(1, "history length " + std::to_string(h) + " exceeds executor capacity " + std::to_string(e->H_bkt));
-    if (c < 1 || c > e->c_bkt)
-      return fail(1, "candidate count " + std::to_string(c) + " outside [1, " + std::to_string(e->c_bkt) + "]");
-    if (h > 0 && !hist_flat) return fail(1, "null argument");
-  }
-  long long* hh = const_cast<long long*>(st.h_hist_ids);
-  long long* hc = const_cast<long long*>(st.h_cand_ids);
-  int* meta = static_cast<int*>(const_cast<void*>(st.h_meta));  // [4][R]: hist len, cand len, out offset, active
-  std::memset(meta, 0, 4 * sizeof(int) * e->R);
-  long long rows = 0;
-  for (int i = 0; i < n_req; ++i) {
-    const long long k = idx[i], h = hist_len[k], c = cand_len[k];
-    if (h) std::memcpy(hh + static_cast<long long>(i) * e->H_bkt, hist_flat + hist_off[k], h * sizeof(long long));
-    std::memcpy(hc + static_cast<long long>(i) * e->c_bkt, cand_flat + cand_off[k], c * sizeof(long long));
-    meta[i] = static_cast<int>(h);
-    meta[e->R + i] = static_cast<int>(c);
-    meta[2 * e->R + i] = static_cast<int>(rows);
-    rows += c;
-  }
-  meta[3 * e->R] = n_req;
-  *n_score_rows = rows;
-  return flame_exec_submit(e, FLAME_INPUT_IDS, n_req, rows, stream);
-}
-
 int flame_exec_wait(FlameExec* e) {
   if (!e || !e->done_ev) return fail(1, "nothing submitted");
   CUDA_TRY(cudaEventSynchronize(e->done_ev));

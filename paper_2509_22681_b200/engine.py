@@ -416,27 +416,6 @@ class DeviceExecutor:
             self._native = False
         self._pending = self._counts
 
-    def submit_gathered(self, batch, idx) -> None:
-        """Id-path ``submit`` of the requests ``idx`` of a whole batch prepared once
-        by ``gather_batch`` (flat ids + offsets + lengths): staging, metadata,
-        validation and the submit are one C call (flame_exec_submit_ids_gather),
-        so the DSO's per-group host work does not grow with the group's size."""
-        if self._pending is not None:
-            raise RuntimeError("executor has an uncollected batch")
-        if not self.with_ids:
-            raise RuntimeError("executor was built without id buffers")
-        hflat, hoff, hl, cflat, coff, cl = batch
-        idx = np.ascontiguousarray(idx, dtype=np.int64)
-        rows = ctypes.c_longlong(0)
-        _lib.check(self.engine.lib.flame_exec_submit_ids_gather(
-            self._ex, hflat.ctypes.data, hoff.ctypes.data, hl.ctypes.data, cflat.ctypes.data, coff.ctypes.data,
-            cl.ctypes.data, idx.ctypes.data, idx.size, ctypes.byref(rows), ctypes.c_void_p(self.stream.cuda_stream)))
-        self.n_real = rows.value
-        self._counts = cl[idx]
-        self._graph_mode = _lib.INPUT_IDS
-        self._native = True
-        self._pending = self._counts
-
     @property
     def pending(self) -> bool:
         return self._pending is not None
@@ -508,36 +487,6 @@ class DeviceExecutor:
         if self._finalizer.alive:
             self.stream.synchronize()
             self._finalizer()
-
-
-def gather_batch(requests) -> tuple:
-    """A batch of (history ids, candidate ids) requests as flat int64 arrays with
-    per-request offsets and lengths: (hist_flat, hist_off, hist_len, cand_flat,
-    cand_off, cand_len), the input of ``DeviceExecutor.submit_gathered``."""
-    n = len(requests)
-    hs = [h for h, _ in requests]
-    cs = [c for _, c in requests]
-    hl = np.fromiter(map(len, hs), dtype=np.int64, count=n)
-    cl = np.fromiter(map(len, cs), dtype=np.int64, count=n)
-
-    def flat(parts, lens):
-        if not n:
-            return np.zeros(0, dtype=np.int64)
-        try:
-            out = np.concatenate(parts, dtype=np.int64, casting="unsafe")  # 1-D id arrays: one C loop
-        except ValueError:  # mixed shapes (e.g. empty 2-D records): flatten one by one
-            out = np.concatenate([np.asarray(a, dtype=np.int64).reshape(-1) for a in parts])
-        if out.size != int(lens.sum()):
-            raise ValueError("id lists must be one-dimensional")
-        return out
-
-    hflat, cflat = flat(hs, hl), flat(cs, cl)
-    hoff = np.zeros(n, dtype=np.int64)
-    coff = np.zeros(n, dtype=np.int64)
-    if n > 1:
-        np.cumsum(hl[:-1], out=hoff[1:])
-        np.cumsum(cl[:-1], out=coff[1:])
-    return hflat, hoff, hl, cflat, coff, cl
 
 
 def _split_rows(flat: np.ndarray, counts) -> list[np.ndarray]:
