@@ -470,11 +470,11 @@ def run_ours(args, dist) -> None:
     name = args.workload
     d, dh, nb, L, f, tasks, H, C, R_default, desc = WORKLOADS[name]
     R = args.requests or R_default
-    dev = torch.device("cuda", dist.local_rank)
+    dev = torch.device("cuda", dist.device_index)
     torch.cuda.set_device(dev)
     cfg = model_config(name)
     params = fb.init_params(cfg)
-    eng = fb.FlameEngine(params, cfg, precision="bf16", device=dist.local_rank)
+    eng = fb.FlameEngine(params, cfg, precision="bf16", device=dist.device_index)
     eng.set_table(build_item_table(NUM_ITEMS, d, STORE_SEED), dtype="fp32")
     reqs = make_requests(R, H, C, WORKLOAD_SEED + dist.rank)
     ex = eng.executor(R, H // nb, C, with_ids=True)
@@ -597,10 +597,10 @@ def run_dso(args, dist) -> None:
     name = args.workload
     d, dh, nb, L, f, tasks, H, C, R_default, desc = WORKLOADS[name]
     R = args.requests or R_default
-    dev = torch.device("cuda", dist.local_rank)
+    dev = torch.device("cuda", dist.device_index)
     torch.cuda.set_device(dev)
     cfg = model_config(name)
-    eng = fb.FlameEngine(fb.init_params(cfg), cfg, precision="bf16", device=dist.local_rank)
+    eng = fb.FlameEngine(fb.init_params(cfg), cfg, precision="bf16", device=dist.device_index)
     eng.set_table(build_item_table(NUM_ITEMS, d, STORE_SEED), dtype="fp32")
     reqs = make_requests(R, H, C, WORKLOAD_SEED + dist.rank, zipf_c=True)
     counts = [len(c) for _, c in reqs]

@@ -51,9 +51,16 @@ class Dist:
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
         self.enabled = self.world_size > 1
         self.backend = backend
+        # FLAME_SHARE_GPU=1 (tests of the multi-rank path on a box with fewer GPUs
+        # than ranks): ranks share GPUs round-robin and the plumbing runs over
+        # gloo, since NCCL needs one GPU per rank.  Production runs one rank per GPU.
+        n_dev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        self.shared_gpu = (os.environ.get("FLAME_SHARE_GPU") == "1" and n_dev > 0
+                           and self.world_size > n_dev)
+        self.device_index = self.local_rank % n_dev if self.shared_gpu else self.local_rank
         if self.enabled and not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            be = backend or ("nccl" if torch.cuda.is_available() else "gloo")
+            be = backend or ("nccl" if torch.cuda.is_available() and not self.shared_gpu else "gloo")
             self.backend = be
             if be == "nccl":
                 torch.cuda.set_device(self.local_rank)
@@ -69,7 +76,7 @@ class Dist:
         """Max over ranks of a scalar (e.g. the timed-region duration)."""
         if not self.enabled:
             return float(value)
-        dev = torch.device("cuda", self.local_rank) if self.backend == "nccl" else torch.device("cpu")
+        dev = torch.device("cuda", self.device_index) if self.backend == "nccl" else torch.device("cpu")
         t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
@@ -77,7 +84,7 @@ class Dist:
     def sum(self, value: float) -> float:
         if not self.enabled:
             return float(value)
-        dev = torch.device("cuda", self.local_rank) if self.backend == "nccl" else torch.device("cpu")
+        dev = torch.device("cuda", self.device_index) if self.backend == "nccl" else torch.device("cpu")
         t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
