@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(fattn::kThreads, 1) sumi_fused_tcgen05(
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::griddep_wait();  // PDL: previous kernel's outputs visible from here on
+  ptx::griddep_launch();
 
   // Unit k of this CTA: u = blockIdx.x + k * gridDim.x -> (r, g, h); its work:
   // pairs of 128-row tiles over the request's REAL candidates (C_r), history

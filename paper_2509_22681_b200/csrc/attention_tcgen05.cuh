@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(attn::kThreads, 1) sumi_attention_tcgen05(
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::griddep_wait();  // PDL: previous kernel's outputs visible from here on
+  ptx::griddep_launch();
 
   // warpgroup i owns whole units: its k-th job is tile k % n_tiles of the CTA's
   // unit number i + 2 * (k / n_tiles), i.e. u = blockIdx.x + that * gridDim.x; a

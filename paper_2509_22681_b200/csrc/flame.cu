@@ -628,9 +628,11 @@ struct Pipe {
         return fail(2, "tensor map for attention output failed");
       a.store_tma = ((hist ? e->hb_bkt : e->c_bkt) % 128) == 0;
       if (hist)
-        sumi_attention_tcgen05<true><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, tm_out, a);
+        CUDA_TRY(launch_pdl(sumi_attention_tcgen05<true>, tgrid, dim3(attn::kThreads), attn::kSmemBytes, s, tm,
+                            tm_out, a));
       else
-        sumi_attention_tcgen05<false><<<tgrid, attn::kThreads, attn::kSmemBytes, s>>>(tm, tm_out, a);
+        CUDA_TRY(launch_pdl(sumi_attention_tcgen05<false>, tgrid, dim3(attn::kThreads), attn::kSmemBytes, s, tm,
+                            tm_out, a));
     } else {
       AttnArgsSimt<float> a{};
       a.qkv = act(e->QKV); a.out = act(e->AO);
@@ -681,7 +683,7 @@ struct Pipe {
     if (ae != cudaSuccess) return fail(2, std::string("fused attention attributes: ") + cudaGetErrorString(ae));
     const int units = e->R * G * c->nh;
     dim3 grid(units < c->num_sms ? units : c->num_sms);
-    sumi_fused_tcgen05<<<grid, fattn::kThreads, fattn::kSmemBytes, s>>>(ta, tw, tq, to, fa);
+    CUDA_TRY(launch_pdl(sumi_fused_tcgen05, grid, dim3(fattn::kThreads), fattn::kSmemBytes, s, ta, tw, tq, to, fa));
     return check();
   }
 
@@ -752,7 +754,7 @@ struct Pipe {
       mark("pda_gather", 0.0, static_cast<double>(e->R) * c->D *
                                   (e->H_bkt * (tab + row_bytes) + e->c_bkt * (tab + 4.0 + (e->Ecc ? 2.0 : 0.0))));
       const int chunks = (c->D + 127) / 128;
-#define PDA_GATHER(T, K) pda_gather<T, K><<<grid, 256, 0, s>>>(g)
+#define PDA_GATHER(T, K) CUDA_TRY(launch_pdl(pda_gather<T, K>, grid, dim3(256), 0, s, g))
 #define PDA_GATHER_T(T)                                                   \
   switch (chunks) {                                                       \
     case 1: PDA_GATHER(T, 1); break;                                      \
@@ -964,9 +966,10 @@ struct Pipe {
                         EPI_BIAS | EPI_GELU | EPI_ROWDOT | (kFold ? EPI_TF32 : 0))) return rc;
       const int n_parts = gemm_row_parts(F, EPI_BIAS | EPI_GELU | EPI_ROWDOT);
       mark("expert_combine", 0.0, static_cast<double>(Rc) * n_parts * c->tasks * 4.0);
-      expert_combine<<<static_cast<unsigned>((Rc + 255) / 256), 256, 0, s>>>(
-          e->partial, n_parts, c->tasks, c->be2, e->c_bkt, e->io.cand_len, e->io.out_offset, e->io.scores,
-          static_cast<int>(Rc));
+      CUDA_TRY(launch_pdl(expert_combine, dim3(static_cast<unsigned>((Rc + 255) / 256)), dim3(256), 0, s,
+                          static_cast<const float*>(e->partial), n_parts, c->tasks, static_cast<const float*>(c->be2),
+                          e->c_bkt, static_cast<const int*>(e->io.cand_len), static_cast<const int*>(e->io.out_offset),
+                          e->io.scores, static_cast<int>(Rc)));
       if (int rc = check()) return rc;
     } else {
       if (int rc = gemm(reinterpret_cast<const Act*>(e->Fz), D, 0, 1, reinterpret_cast<const Act*>(c->we1), D, 0,

@@ -22,6 +22,42 @@ struct GemmProblem {
   int epi;  // EPI_* flags
 };
 
+// Programmatic dependent launch for the kernels of a forward pass (FLAME_PDL=1;
+// off by default: measured neutral): each such kernel runs its
+// prologue (barrier init, TMEM allocation, tensor-map prefetch) while its
+// predecessor drains, then waits in ptx::griddep_wait() for the predecessor's
+// results.  Only kernels that execute griddep_wait() before touching predecessor
+// data may be launched this way.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("FLAME_PDL");
+    return v && atoi(v) == 1;
+  }();
+  return on;
+}
+
+inline void pdl_attr(cudaLaunchAttribute& at) {
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t q = {};
+  cudaLaunchAttribute at[1];
+  q.gridDim = grid;
+  q.blockDim = block;
+  q.dynamicSmemBytes = smem;
+  q.stream = s;
+  if (pdl_enabled()) {
+    pdl_attr(at[0]);
+    q.attrs = at;
+    q.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&q, kernel, args...);
+}
+
 // CTA pairs (cta_group::2, 256-row tiles) unless FLAME_GEMM_CLUSTER=1
 static int gemm_cluster_pref() {
   static int v = [] {
@@ -122,14 +158,13 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   if (ncl == 1) {
     const int total = p.G * m_tiles * n_tiles;
     const int grid = total < num_sms ? total : num_sms;
-    gemm_bf16_tcgen05<BN, EPI, 1><<<grid, C1::kThreads, C1::kSmemBytes, s>>>(
-        ta, tb, to, to2, tr, p.K / kBKe, m_tiles, n_tiles, p.G, p.a_shared, ep);
-    return cudaGetLastError();
+    return launch_pdl(gemm_bf16_tcgen05<BN, EPI, 1>, dim3(grid), dim3(C1::kThreads), C1::kSmemBytes, s, ta, tb,
+                      to, to2, tr, p.K / kBKe, m_tiles, n_tiles, p.G, p.a_shared, ep);
   }
   const int total_pairs = p.G * ((m_tiles + 1) / 2) * n_tiles;
   const int clusters = total_pairs < max_clusters ? total_pairs : max_clusters;
   cudaLaunchConfig_t q = {};
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
@@ -140,6 +175,7 @@ static cudaError_t launch_gemm_t(const GemmProblem& p, cudaStream_t s, int num_s
   q.stream = s;
   q.attrs = at;
   q.numAttrs = 1;
+  if (pdl_enabled()) pdl_attr(at[q.numAttrs++]);
   return cudaLaunchKernelEx(&q, gemm_bf16_tcgen05<BN, EPI, 2>, ta, tb, to, to2, tr, p.K / kBKe, m_tiles, n_tiles,
                             p.G, p.a_shared, ep);
 }

@@ -285,6 +285,10 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   if constexpr (kCG > 1) ptx::cluster_sync();  // peer barriers / TMEM ready before any pair MMA
+  // PDL: the prologue above overlapped the previous kernel's tail; its outputs
+  // (A operand, residual, row statistics) are read only after this
+  ptx::griddep_wait();
+  ptx::griddep_launch();
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer

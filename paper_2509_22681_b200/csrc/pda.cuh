@@ -59,6 +59,7 @@ struct PdaLists {
 // at 100k items: 5 passes instead of 16).
 template <int kThreads, int kItems>
 __global__ void __launch_bounds__(kThreads) pda_dedup(PdaLists a) {
+  ptx::griddep_launch();  // let pda_gather's CTAs launch as this grid drains
   using Sort = cub::BlockRadixSort<unsigned long long, kThreads, kItems, int>;
   constexpr int P = kThreads * kItems;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -276,6 +277,8 @@ __device__ __forceinline__ void assemble_row_st(const AssembleOut& o, bool hist,
 // resident CTAs per SM: the kernel is memory-latency bound.
 template <typename TTab, int kChunks>
 __global__ void __launch_bounds__(256) pda_gather(PdaGatherArgs a) {
+  ptx::griddep_wait();  // PDL: pda_dedup's unique lists / work list
+  ptx::griddep_launch();
   const int seg_list = blockIdx.y;  // (list, segment) of pda_dedup
   const int list = seg_list / a.l.nseg, seg = seg_list % a.l.nseg;
   const bool is_hist = list < a.l.R;

@@ -49,6 +49,14 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
+// Programmatic dependent launch (PTX ISA griddepcontrol).  wait: block until every
+// prerequisite grid has completed and its memory is visible (a no-op when the
+// kernel was launched without the programmatic-serialization attribute).
+// launch_dependents: this CTA no longer holds back the next PDL-launched grid,
+// whose CTAs may then start their prologue on SMs this grid has left.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

@@ -211,6 +211,8 @@ __device__ __forceinline__ void store_centered(__nv_bfloat16* y, const float4 (&
 __global__ void expert_combine(const float* __restrict__ partial, int n_parts, int tasks,
                                const float* __restrict__ b2, int c_bkt, const int* __restrict__ cand_len,
                                const int* __restrict__ out_offset, float* __restrict__ out, int rows) {
+  ptx::griddep_wait();  // PDL: the expert GEMM's row-dot partials
+  ptx::griddep_launch();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= rows) return;
   const int r = row / c_bkt, c = row % c_bkt;
