@@ -169,6 +169,8 @@ struct FlameExec {
   float* Xb = nullptr;
   void* Fz = nullptr;
   void* He = nullptr;
+  float* gpart = nullptr;      // gated W2 hand-over sums: [num_sms][8 epilogue warps][32 x 128] fp32
+  int* gflag = nullptr;        // and their flags [num_sms][8] (zero between launches)
   void* Ehc = nullptr;         // bf16 path: centered history rows [G][Rh][D]
   void* Ecc = nullptr;         // bf16 path: centered candidate rows [Rc][D]
   float* rs_h = nullptr;       // rstd of the history rows [G][Rh]
@@ -509,6 +511,7 @@ struct Pipe {
     ep.lnstats = ln.lnstats; ep.lnstats_gstride = ln.lnstats_gstride; ep.stats_parts = ln.stats_parts;
     ep.d_true = ln.d_true; ep.colsum = ln.colsum; ep.colsum_gstride = ln.colsum_gstride;
     ep.resid_b = resid_b; ep.gate_w = gate_w; ep.gate_b = gate_b;
+    if (gate_w != nullptr) { ep.gpart = e->gpart; ep.gflag = e->gflag; }  // balanced gated schedule
     if (e->io.active != nullptr && e->R > 0 && (M == e->Rh || M == e->Rc) && M % e->R == 0) {
       // a slot-major row range (all history rows or all candidate rows): skip unused slots
       ep.m_active = e->io.active;
@@ -1248,6 +1251,12 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
   e->Xa = static_cast<float*>(A(G * rows * D * 4));
   e->Xb = c->L > 1 ? static_cast<float*>(A(G * rows * D * 4)) : nullptr;
   e->Fz = A(e->Rc * D * 4);  // fp32 fused rows (both modes)
+  if (fold && gated_bn256()) {
+    const size_t slots = static_cast<size_t>(c->num_sms) * 8;
+    e->gpart = static_cast<float*>(A(slots * 32 * 128 * 4));
+    e->gflag = static_cast<int*>(A(slots * 4));
+    if (e->gflag != nullptr && cudaMemset(e->gflag, 0, slots * 4) != cudaSuccess) ok = false;
+  }
   e->He = (fold && c->tasks <= 4) ? nullptr : A(e->Rc * F * 4);
   const size_t lists = 2 * static_cast<size_t>(R) * nseg;  // (list, segment) slots
   e->spos = static_cast<int*>(A(lists * cap * 4));

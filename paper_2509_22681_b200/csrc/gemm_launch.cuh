@@ -58,6 +58,16 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&q, kernel, args...);
 }
 
+// gated-fusion W2 at BN = 256 (opt-in, FLAME_GATED_BN=256); executors allocate its
+// hand-over scratch only when it is on
+inline bool gated_bn256() {
+  static const bool on = [] {
+    const char* v = getenv("FLAME_GATED_BN");
+    return v && atoi(v) == 256;
+  }();
+  return on;
+}
+
 // CTA pairs (cta_group::2, 256-row tiles) unless FLAME_GEMM_CLUSTER=1
 static int gemm_cluster_pref() {
   static int v = [] {
@@ -238,6 +248,9 @@ static cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t s, int num_sms
   constexpr int kGatedW2 = EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_GATED;
   if (p.epi & EPI_GATED) {
     if (p.epi != kGatedW2 || p.N % 32 != 0) return cudaErrorInvalidValue;
+    // FLAME_GATED_BN=256: BN = 256 with the running sum in registers and the
+    // balanced hand-over schedule (measured neutral at cfg3)
+    if (p.N >= 256 && gated_bn256()) return launch_gemm_t<256, kGatedW2>(p, s, num_sms);
     return launch_gemm_t<128, kGatedW2>(p, s, num_sms);
   }
   if (p.N >= 256) return launch_gemm_bn<256>(p, s, num_sms);

@@ -68,6 +68,13 @@ struct GemmEpilogue {
   // reaches HBM, as the fp32 operand of the tf32 expert GEMM ([M][N])
   const float* gate_w;    // [G][N]
   const float* gate_b;    // [G][N]
+  // balanced gated schedule (BN = 256, sum in registers): a cluster may end inside
+  // a chain of groups and hand its running sum to the next cluster, which finishes
+  // that chain last.  Scratch per (cluster, CTA, epilogue warp): the sum rows
+  // (32 lanes x kMyChunks x 32 fp32) and a flag (0 / 1, reset by the consumer).
+  // Null: whole chains per cluster.
+  float* gpart;
+  int* gflag;
   // device-side active row count (DSO executors): rows >= *m_active * rows_per_slot
   // are unused slots and their tiles are skipped (null: all M rows)
   const int* m_active;
@@ -144,8 +151,14 @@ struct Cfg {
   static constexpr bool kF32 = (EPI & EPI_OUT_F32) != 0;
   static constexpr bool kRowDot = (EPI & EPI_ROWDOT) != 0;
   static constexpr bool kGated = (EPI & EPI_GATED) != 0;
-  static_assert(!kGated || (BN == 128 && !kF32 && (EPI & EPI_RESID_BF16) != 0),
-                "gated-fusion epilogue: BN = 128, bf16 output, bf16 residual");
+  static_assert(!kGated || ((BN == 128 || BN == 256) && !kF32 && (EPI & EPI_RESID_BF16) != 0),
+                "gated-fusion epilogue: BN = 128 / 256, bf16 output, bf16 residual");
+  // gated fusion at BN = 256: both TMEM halves hold accumulators, so the running
+  // sum over groups lives in the epilogue threads' registers (kMyChunks x 32 fp32
+  // per thread), paid for by setmaxnreg (kRegsEpi for the epilogue warpgroups,
+  // kRegsCtl for the producer / MMA warpgroup; together the launch allocation)
+  static constexpr bool kRegSum = kGated && BN == 256;
+  static constexpr int kRegsEpi = 232, kRegsCtl = 40;
   // STATS with an fp32 primary output, and the gated sum (hi + lo halves), also
   // stage a second bf16 box
   static constexpr bool kDual = (EPI & EPI_STATS) != 0 && kF32;
@@ -237,10 +250,38 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   const int cid = blockIdx.x / ncl;
   const int nclusters = gridDim.x / ncl;
   const int total_tiles = groups * m_pairs * n_tiles;
+  // Balanced gated schedule: the chains of G group tiles laid end to end and cut
+  // into nclusters equal ranges.  A range may end inside a chain (its TAIL piece:
+  // groups [0, e % G) of chain e / G, worked FIRST, its running sum handed over
+  // through ep.gpart) and begin inside one (its HEAD piece: groups [b % G, G) of
+  // chain b / G, worked LAST, continuing the previous cluster's sum); whole chains
+  // in between.  The fp32 sum still runs over the groups in order.  Chains are
+  // numbered n-block-major, so clusters k and k + S / n_tiles work the same rows
+  // (the shared A tiles) at the same time and those re-reads hit L2.
+  bool bal = false;
+  int bt_nt = 0, bt_st = 0, bt_sa = 0, bt_nf = 0, bt_nh = 0, bt_sh = 0, bt_gh = 0;
+  if constexpr (C::kRegSum) {
+    const long long T = static_cast<long long>(groups) * m_pairs * n_tiles;
+    if (ep.gpart != nullptr && T / nclusters >= 2 * groups) {
+      bal = true;
+      const int b = static_cast<int>(cid * T / nclusters), e = static_cast<int>((cid + 1) * T / nclusters);
+      bt_nt = e % groups;
+      bt_st = e / groups;
+      bt_sa = (b + groups - 1) / groups;
+      bt_nf = (e / groups - bt_sa) * groups;
+      bt_gh = b % groups;
+      bt_nh = bt_gh != 0 ? groups - bt_gh : 0;
+      bt_sh = b / groups;
+    }
+  }
   // tile -> (group, m pair, n block).  Group-fastest order when every group reads
   // the same A rows or residual tile: the G consecutive tiles hit it in L2.
   auto decode = [&](int t, int& g, int& mp, int& nb) {
-    if (C::kGated || ep.g_inner) {
+    if (C::kRegSum && bal) {
+      g = t % groups;
+      nb = (t / groups) / m_pairs;
+      mp = (t / groups) % m_pairs;
+    } else if (C::kGated || ep.g_inner) {
       g = t % groups;
       nb = (t / groups) % n_tiles;
       mp = t / (groups * n_tiles);
@@ -254,6 +295,12 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   // cluster owns whole (m pair, n block) super tiles and walks their groups in order
   auto tile_at = [&](int it) -> int {
     if constexpr (C::kGated) {
+      if (bal) {
+        if (it < bt_nt) return bt_st * groups + it;
+        const int j = it - bt_nt;
+        if (j < bt_nf) return bt_sa * groups + j;
+        return j - bt_nf < bt_nh ? bt_sh * groups + bt_gh + (j - bt_nf) : total_tiles;
+      }
       const int st = cid + (it / groups) * nclusters;
       return st < m_pairs * n_tiles ? st * groups + it % groups : total_tiles;
     } else {
@@ -289,7 +336,14 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   // (A operand, residual, row statistics) are read only after this
   ptx::griddep_wait();
   ptx::griddep_launch();
+  static_assert(!C::kRegSum || (C::kThreads == 384 && 128 * C::kRegsCtl + 256 * C::kRegsEpi <= 384 * 168),
+                "setmaxnreg budget above the launch allocation");
 
+  // warpgroup 0: producer (warp 0), MMA issuer (warp 1 of the even CTA), TMEM
+  // allocator (warp 2); warpgroups 1-2: epilogue.  setmaxnreg is executed per
+  // warpgroup, before the warps split into roles
+  if (warp < 4) {
+  if constexpr (C::kRegSum) ptx::setmaxnreg_dec<C::kRegsCtl>();
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     // whole warp walks the schedule (operands stay warp-uniform); one lane issues
@@ -396,7 +450,9 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       GEMM_TRACE(0, 3);
       if (++acc == C::kAcc) { acc = 0; acc_phase ^= 1; }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    if constexpr (C::kRegSum) ptx::setmaxnreg_inc<C::kRegsEpi>();
     // ----------------------------------------------------------- epilogue
     constexpr bool kF32 = C::kF32;
     constexpr int kChunks = C::kChunks;
@@ -490,6 +546,8 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
       return o;
     };
     RowOps row_ops = load_row_ops(tile_at(0));
+    // kRegSum: this thread's row of the running gated sum, chunk k at gsum[k]
+    float gsum[C::kRegSum ? C::kMyChunks : 1][32];
     for (int it = 0, tile = tile_at(0); tile < total_tiles; tile = tile_at(++it)) {
       int g, mp, n_blk;
       decode(tile, g, mp, n_blk);
@@ -568,7 +626,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         }
         float v[32];
         uint32_t gs[32];  // gated running sum of this chunk (groups < g)
-        if constexpr (C::kGated) {
+        if constexpr (C::kGated && !C::kRegSum) {
           if (!g_first) {
             ptx::tmem_ld_32x32b_x32(t_gsum + c * 32, gs);
             ptx::tmem_ld_wait();
@@ -667,8 +725,13 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
             p0 = f2::mul(p0, f2::make(sigmoid_fast(a0), sigmoid_fast(a1)));
             p1 = f2::mul(p1, f2::make(sigmoid_fast(a2), sigmoid_fast(a3)));
             if (!g_first) {
-              p0 = f2::add(f2::make(__uint_as_float(gs[j]), __uint_as_float(gs[j + 1])), p0);
-              p1 = f2::add(f2::make(__uint_as_float(gs[j + 2]), __uint_as_float(gs[j + 3])), p1);
+              if constexpr (C::kRegSum) {
+                p0 = f2::add(f2::make(gsum[k][j], gsum[k][j + 1]), p0);
+                p1 = f2::add(f2::make(gsum[k][j + 2], gsum[k][j + 3]), p1);
+              } else {
+                p0 = f2::add(f2::make(__uint_as_float(gs[j]), __uint_as_float(gs[j + 1])), p0);
+                p1 = f2::add(f2::make(__uint_as_float(gs[j + 2]), __uint_as_float(gs[j + 3])), p1);
+              }
             }
           }
           if constexpr ((EPI & EPI_STATS) != 0) {
@@ -689,6 +752,9 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
             dot01 = f2::fma(vv, f2::make(w.x, w.y), dot01);
             dot23 = f2::fma(vv, f2::make(w.z, w.w), dot23);
           }
+        } else if (C::kRegSum && !g_last) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) gsum[C::kRegSum ? k : 0][j] = v[j];  // carried in registers
         } else if (C::kGated && !g_last) {
           // carry the running sum to the next group's tile (same thread, same lanes)
 #pragma unroll
@@ -735,6 +801,61 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         }
       };
 
+      // balanced schedule hand-over slots of this warp (see bal above)
+      const bool from_part = C::kRegSum && bal && bt_nh > 0 && it == bt_nt + bt_nf;
+      const bool to_part = C::kRegSum && bal && bt_nt > 0 && it == bt_nt - 1;
+      if constexpr (C::kRegSum) {
+        if (from_part) {
+          // the previous cluster's running sum over groups [0, g) of this chain; it
+          // made it as its first work, so the wait is normally already satisfied
+          const long long slot = ((static_cast<long long>(cid - 1) * ncl + crank) * kEpiWarps + ew);
+          int* fl = ep.gflag + slot;
+          if (lane == 0) {
+            long long spins = 0;
+            while (ptx::ld_acquire_gpu(fl) == 0) {
+              __nanosleep(64);
+              if (++spins > (1LL << 26)) __trap();  // a lost hand-over must fail, not hang
+            }
+            *fl = 0;  // single consumer: ready for the next launch
+          }
+          __syncwarp();
+          const float4* src = reinterpret_cast<const float4*>(ep.gpart + slot * (32 * C::kMyChunks * 32)) +
+                              lane * (C::kMyChunks * 8);
+#pragma unroll
+          for (int k = 0; k < C::kMyChunks; ++k)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 t4 = __ldcg(src + k * 8 + q);
+              gsum[k][4 * q] = t4.x; gsum[k][4 * q + 1] = t4.y; gsum[k][4 * q + 2] = t4.z; gsum[k][4 * q + 3] = t4.w;
+            }
+        }
+      }
+      if constexpr (C::kRegSum) {
+        // fully unrolled, so gsum is indexed statically (registers, not local
+        // memory); the 16k-cycle K = 2048 mainloop hides the unpipelined loads
+#pragma unroll
+        for (int k = 0; k < C::kMyChunks; ++k) {
+          if (half + k * kEpiPerQuad < kChunks) {
+            uint32_t rr[32];
+            ptx::tmem_ld_32x32b_x32(t_row + (half + k * kEpiPerQuad) * 32, rr);
+            ptx::tmem_ld_wait();
+            chunk(k, rr);
+          }
+        }
+        if (to_part) {
+          // hand the sum over groups [0, g] to the next cluster (its head piece)
+          const long long slot = ((static_cast<long long>(cid) * ncl + crank) * kEpiWarps + ew);
+          float4* dst = reinterpret_cast<float4*>(ep.gpart + slot * (32 * C::kMyChunks * 32)) + lane * (C::kMyChunks * 8);
+#pragma unroll
+          for (int k = 0; k < C::kMyChunks; ++k)
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              __stcg(dst + k * 8 + q, make_float4(gsum[k][4 * q], gsum[k][4 * q + 1], gsum[k][4 * q + 2], gsum[k][4 * q + 3]));
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) ptx::st_release_gpu(ep.gflag + slot, 1);
+        }
+      } else {
       // TMEM chunks ping-pong between two register sets: the load of chunk k+1
       // is in flight while chunk k is processed
       uint32_t ra[32], rb[32];
@@ -751,6 +872,7 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
         if (has2) ptx::tmem_ld_32x32b_x32(t_row + (half + (k + 2) * kEpiPerQuad) * 32, ra);
         chunk(k + 1, rb);
         if (!has2) break;
+      }
       }
       if constexpr ((EPI & EPI_STATS) != 0) {
         if (row0 + lane < ep.M) {
