@@ -19,11 +19,22 @@ ex = eng.executor(R, H // nb, C, with_ids=True)
 ex.stage_ids(reqs); ex.run(_lib.INPUT_IDS, graph=False); ex.stream.synchronize()
 lib = _lib.load()  # needs a FLAME_DEBUG_TRACE build: FLAME_B200_LIB=dev/var_trace.so (dev/build_variant.sh trace -DFLAME_DEBUG_TRACE)
 lib.flame_debug_gemm_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = torch.zeros(4 * 4096, dtype=torch.int64, device="cuda")
+buf = torch.zeros(4 * 4096 + 2 * 1024, dtype=torch.int64, device="cuda")
 lib.flame_debug_gemm_trace(ctypes.c_void_p(buf.data_ptr()), which)
 ex.run(_lib.INPUT_IDS, graph=False); ex.stream.synchronize()
 lib.flame_debug_gemm_trace(None, -1)
-t = buf.cpu().numpy().astype(np.uint64).reshape(4, 4096)
+allb = buf.cpu().numpy().astype(np.uint64)
+t = allb[:4 * 4096].reshape(4, 4096)
+se = allb[4 * 4096:].reshape(-1, 2)
+se = se[(se[:, 0] > 0) & (se[:, 1] > 0)].astype(np.int64)
+if len(se):
+    g0 = se[:, 0].min()
+    st, en = (se[:, 0] - g0) / 1e3, (se[:, 1] - g0) / 1e3
+    print(f"CTAs {len(se)}: start us min/max {st.min():.1f}/{st.max():.1f}; end us min/p10/p50/p90/max "
+          f"{en.min():.1f}/{np.percentile(en, 10):.1f}/{np.median(en):.1f}/{np.percentile(en, 90):.1f}/{en.max():.1f}")
+    order = np.argsort(en)
+    print("  slowest CTAs (index: end us):", " ".join(f"{i}:{en[i]:.0f}" for i in order[-8:]))
+    print("  fastest CTAs (index: end us):", " ".join(f"{i}:{en[i]:.0f}" for i in order[:8]))
 names = {1: "M:acc_free", 2: "M:data", 3: "M:commit", 4: "E:full", 5: "E:chunk", 6: "E:free", 7: "P:stage", 8: "E:resid", 9: "E:staged", 10: "M:kb_data", 11: "M:kb_wait"}
 t0 = min(int(x >> 8) for row in t for x in row if x)
 for slot in range(4):

@@ -336,6 +336,14 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
   // (A operand, residual, row statistics) are read only after this
   ptx::griddep_wait();
   ptx::griddep_launch();
+#ifdef FLAME_DEBUG_TRACE
+  // per-CTA start / end (globaltimer ns) after the 4 x 4096 per-event slots
+  if (g_gemm_trace != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_trace[4 * 4096 + 2 * blockIdx.x] = t;
+  }
+#endif
   static_assert(!C::kRegSum || (C::kThreads == 384 && 128 * C::kRegsCtl + 256 * C::kRegsEpi <= 384 * 168),
                 "setmaxnreg budget above the launch allocation");
 
@@ -916,6 +924,13 @@ __global__ void __launch_bounds__(gemm::Cfg<BN, EPI, kCG>::kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc_cg<C::kTmemCols, kCG>(tmem_base);
   }
+#ifdef FLAME_DEBUG_TRACE
+  if (g_gemm_trace != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_trace[4 * 4096 + 2 * blockIdx.x + 1] = t;
+  }
+#endif
 }
 
 }  // namespace flame
