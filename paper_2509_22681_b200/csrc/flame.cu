@@ -1251,7 +1251,7 @@ int flame_exec_create(FlameCtx* c, int R, int hb_bkt, int c_bkt, const FlameIO* 
   e->Xa = static_cast<float*>(A(G * rows * D * 4));
   e->Xb = c->L > 1 ? static_cast<float*>(A(G * rows * D * 4)) : nullptr;
   e->Fz = A(e->Rc * D * 4);  // fp32 fused rows (both modes)
-  if (fold && gated_bn256()) {
+  if (fold && gated_bn256(static_cast<int>(D))) {
     const size_t slots = static_cast<size_t>(c->num_sms) * 8;
     e->gpart = static_cast<float*>(A(slots * 32 * 128 * 4));
     e->gflag = static_cast<int*>(A(slots * 4));

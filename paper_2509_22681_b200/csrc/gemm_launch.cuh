@@ -58,14 +58,25 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&q, kernel, args...);
 }
 
-// gated-fusion W2 at BN = 256 (opt-in, FLAME_GATED_BN=256); executors allocate its
-// hand-over scratch only when it is on
-inline bool gated_bn256() {
-  static const bool on = [] {
+// Gated-fusion W2 tile width: BN = 256 (running sum in registers, balanced
+// hand-over schedule) for N = 256 / 512, BN = 128 (sum in TMEM) otherwise.
+// Measured at cfg3 (N = 512): W2 0.505 -> 0.447 ms, step 2.02 -> 1.95 ms; cfg2
+// (N = 256) step -0.9 %; cfg5 (N = 768) W2 0.44 -> 0.47 ms, so it keeps BN = 128
+// (profiles/r02h/sched_fence_ab).  FLAME_GATED_BN=128 / 256 forces one (A/B).
+// Executors allocate the hand-over scratch only when BN = 256 can be chosen.
+inline int gated_bn_env() {
+  static const int force = [] {
     const char* v = getenv("FLAME_GATED_BN");
-    return v && atoi(v) == 256;
+    return v ? atoi(v) : 0;
   }();
-  return on;
+  return force;
+}
+inline bool gated_bn_forced() { return gated_bn_env() == 256; }
+inline bool gated_bn256(int N) {
+  if (N < 256 || N % 32 != 0) return false;
+  if (gated_bn_env() == 256) return true;
+  if (gated_bn_env() == 128) return false;
+  return N % 256 == 0 && N <= 512;
 }
 
 // CTA pairs (cta_group::2, 256-row tiles) unless FLAME_GEMM_CLUSTER=1
@@ -248,9 +259,11 @@ static cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t s, int num_sms
   constexpr int kGatedW2 = EPI_BIAS | EPI_RESID | EPI_RESID_BF16 | EPI_GATED;
   if (p.epi & EPI_GATED) {
     if (p.epi != kGatedW2 || p.N % 32 != 0) return cudaErrorInvalidValue;
-    // FLAME_GATED_BN=256: BN = 256 with the running sum in registers and the
-    // balanced hand-over schedule (measured neutral at cfg3)
-    if (p.N >= 256 && gated_bn256()) return launch_gemm_t<256, kGatedW2>(p, s, num_sms);
+    // BN = 256 chains are twice as long: only when there are enough of them to
+    // occupy every CTA pair (small DSO groups keep BN = 128's parallelism)
+    const long long chains256 = (static_cast<long long>(p.M) + 255) / 256 * (p.N / 256);
+    if (gated_bn256(p.N) && (chains256 >= num_sms / 2 || gated_bn_forced()))
+      return launch_gemm_t<256, kGatedW2>(p, s, num_sms);
     return launch_gemm_t<128, kGatedW2>(p, s, num_sms);
   }
   if (p.N >= 256) return launch_gemm_bn<256>(p, s, num_sms);

@@ -114,7 +114,21 @@ __device__ unsigned long long* g_gemm_trace = nullptr;
     }                                                                                           \
   } while (0)
 #else
-#define GEMM_TRACE(slot, code) do { (void)gtrace_k; } while (0)
+// Production builds keep a compiler memory barrier at the trace sites of the MMA
+// issuer (slot 0: after the accumulator wait, at the first k-block, after the
+// commit) and of the producer (slot 3: after each stage's empty wait).  Measured:
+// without it ptxas schedules the BN = 256 gated-fusion W2 into 0.51 ms at cfg3,
+// with it 0.445 ms (the debug-trace build, whose trace sites act as the same
+// barriers, had shown the gap; profiles/r02h/sched_fence_ab).  FLAME_PROBE_MASK
+// (bit 0 MMA issuer, 1-2 epilogue, 3 producer) overrides it for A/B builds.
+#ifndef FLAME_PROBE_MASK
+#define FLAME_PROBE_MASK 9
+#endif
+#define GEMM_TRACE(slot, code)                                        \
+  do {                                                                \
+    (void)gtrace_k;                                                   \
+    if ((FLAME_PROBE_MASK >> (slot)) & 1) asm volatile("" ::: "memory"); \
+  } while (0)
 #endif
 
 namespace gemm {

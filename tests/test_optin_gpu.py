@@ -1,9 +1,10 @@
-"""Opt-in kernel variants (read from the environment once per process, so each runs
-in a subprocess) against the reference's golden outputs and the default build:
+"""Kernel variants selected by environment (read once per process, so each runs in a
+subprocess) against the reference's golden outputs and each other:
 
-* FLAME_GATED_BN=256 — gated-fusion W2 at BN = 256 with the running sum in
+* FLAME_GATED_BN=256 / 128 — gated-fusion W2 at BN = 256 with the running sum in
   registers and the balanced cluster schedule with L2 hand-over of partial chains
-  (csrc/gemm_tcgen05.cuh, kRegSum);
+  (csrc/gemm_tcgen05.cuh, kRegSum; the default for N = 256 / 512), forced on for
+  every shape, against BN = 128 with the sum in TMEM forced everywhere;
 * FLAME_PDL=1 — programmatic dependent launch of the forward-pass kernels.
 
 Reference semantics: model/forward.py:143-156 (gated fusion), :186-204.
