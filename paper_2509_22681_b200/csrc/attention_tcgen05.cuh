@@ -66,7 +66,16 @@ __device__ unsigned int g_attn_trace_n[4];
     }                                                                                     \
   } while (0)
 #else
-#define ATTN_TRACE(slot, code) do { (void)trace_k; } while (0)
+// FLAME_ATTN_PROBE_MASK (dev A/B): a compiler memory barrier at the trace sites of
+// the slots in the mask (bits 0-1 softmax warpgroups, 2 MMA issuer, 3 producer)
+#ifndef FLAME_ATTN_PROBE_MASK
+#define FLAME_ATTN_PROBE_MASK 0
+#endif
+#define ATTN_TRACE(slot, code)                                             \
+  do {                                                                     \
+    (void)trace_k;                                                         \
+    if ((FLAME_ATTN_PROBE_MASK >> (slot)) & 1) asm volatile("" ::: "memory"); \
+  } while (0)
 #endif
 
 namespace attn {
