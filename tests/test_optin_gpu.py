@@ -70,3 +70,13 @@ def test_optin_variant_matches_reference_and_default(gpu, default_run, env):
         assert np.abs(np.asarray(scores) - np.asarray(default_run[name][1])).max() <= 1e-3
     ref = np.asarray(default_run["batch"])
     assert np.abs(np.asarray(got["batch"]) - ref).max() <= 1e-3
+
+
+def test_forced_bn256_gated_under_concurrent_dso_groups(gpu):
+    # the balanced hand-over schedule with several executors' graphs in flight on
+    # separate streams at once (the DSO), each with its own scratch and flags
+    env = dict(os.environ, FLAME_GATED_BN="256")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        str(ROOT / "tests" / "test_dso_gpu.py")], cwd=str(ROOT), env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
